@@ -1,0 +1,56 @@
+// Host-side launcher declarations for the spaimg sm_100a kernels (internal to the library).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "spaimg_common.cuh"
+
+namespace spaimg {
+
+Layout make_layout(int dim, int N, int esize);
+
+// dense (n^dim, C order) <-> padded interior
+template <class T> cudaError_t launch_pad(const Layout& L, const T* dense, T* padded, cudaStream_t s);
+template <class T> cudaError_t launch_unpad(const Layout& L, const T* padded, T* dense, cudaStream_t s);
+
+// K0: zero-extended stencil product on dense arrays (any offset radius), stencils.py:136-153
+template <class T>
+cudaError_t launch_apply_dense(int dim, int N, const T* x, T* out, const Terms<T>& terms, T scale,
+                               cudaStream_t s);
+
+// unfused building blocks on padded levels
+template <class T>
+cudaError_t launch_residual(const Layout& L, const T* x, const T* b, T* r, T sA, cudaStream_t s);
+template <class T>
+cudaError_t launch_relax(const Layout& L, const T* x, const T* r, T* xo, const Terms<T>& M, int shape, T sM,
+                         T omega, cudaStream_t s);
+template <class T>
+cudaError_t launch_restrict(const Layout& Lf, const Layout& Lc, const T* r, T* bc, cudaStream_t s);
+
+// K1: fused smoothing sweep x' = x + omega M (b - A x); from_zero => x == 0 (x not read)
+template <class T>
+cudaError_t launch_sweep(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, int shape, T sA,
+                         T sM, T omega, bool from_zero, cudaStream_t s);
+bool sweep_fused_supported(int dim, int shape);
+
+// K2: fused residual + full-weighting restriction
+template <class T>
+cudaError_t launch_residual_restrict(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T sA,
+                                     T* scratch_r, cudaStream_t s);
+// K3: fused prolongation + correction (in place on x); acc=false stores prolong(e) alone
+template <class T>
+cudaError_t launch_prolong_correct(const Layout& Lf, const Layout& Lc, T* x, const T* e, cudaStream_t s,
+                                   bool acc = true);
+
+// K4: deterministic two-stage ||b - A x||_2 into norms[slot] (double); partials/counter scratch
+constexpr int kNormBlocks = 592;  // 4 x 148 SMs
+template <class T>
+cudaError_t launch_residual_norm(const Layout& L, const T* x, const T* b, T sA, double* partials,
+                                 unsigned* counter, double* norms, int slot, int* slot_dev, cudaStream_t s);
+
+// K5: coarse direct solve (LAPACK getrs order, Appendix A.5/A.6)
+template <class T>
+cudaError_t launch_coarse_solve(const Layout& L, const T* b, T* x, const T* lu, const int* piv, int nlu,
+                                cudaStream_t s);
+
+}  // namespace spaimg

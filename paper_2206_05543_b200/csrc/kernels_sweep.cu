@@ -1,0 +1,181 @@
+// K1 fused smoothing sweep and K2 fused residual + restriction.
+//
+// Sweep (reference multigrid.py:98-100 for one step):  r = b - A x on the tile plus a one-point
+// halo in shared memory, then x' = x + omega * ((M r) * sM) from that tile in the same pass.
+// r is forced to zero outside the interior (the reference zero-pads r itself, stencils.py:146).
+#include "kernels.h"
+
+namespace spaimg {
+
+template <class T, int S>
+__device__ __forceinline__ int toff(const Terms<T>& M, int k, int a) {
+    if constexpr (S == SHAPE_GENERIC) {
+        return M.off[k][a];
+    } else {
+        return ShapeT<S>::o(k, a);
+    }
+}
+template <class T, int S>
+__device__ __forceinline__ int tnt(const Terms<T>& M) {
+    if constexpr (S == SHAPE_GENERIC) {
+        return M.nt;
+    } else {
+        return ShapeT<S>::nt;
+    }
+}
+
+__device__ __forceinline__ long long pidx2(const Layout& L, int i0, int i1) { return L.origin + (long long)i0 * L.px + i1; }
+__device__ __forceinline__ long long pidx3(const Layout& L, int i0, int i1, int i2) {
+    return L.origin + (long long)i0 * L.pp + (long long)i1 * L.px + i2;
+}
+
+// ------------------------------------------------------------------------------------------
+// v1 tiles (halo recomputation; row/plane marching versions replace these per dim)
+// ------------------------------------------------------------------------------------------
+constexpr int S2_TW = 64, S2_TH = 16;
+constexpr int S3_TX = 32, S3_TY = 8, S3_TZ = 4;
+
+template <class T, int S, bool FZ>
+__global__ void __launch_bounds__(256) k_sweep2d_tile(Layout L, const T* __restrict__ x, const T* __restrict__ b,
+                                                      T* __restrict__ xo, Terms<T> M, T sA, T sM, T omega) {
+    using O = Op<T>;
+    constexpr int RW = S2_TW + 2, RH = S2_TH + 2;
+    __shared__ T rs[RH * RW];
+    const int c0 = blockIdx.x * S2_TW, r0 = blockIdx.y * S2_TH;
+    const int n = L.n;
+    for (int q = threadIdx.x; q < RH * RW; q += blockDim.x) {
+        const int i0 = r0 - 1 + q / RW, i1 = c0 - 1 + q % RW;
+        T rv = T(0);
+        if (i0 >= 0 && i0 < n && i1 >= 0 && i1 < n) {
+            const long long p = pidx2(L, i0, i1);
+            if constexpr (FZ) {
+                rv = b[p];  // b - A 0 == b exactly
+            } else {
+                rv = residual2d<T>(b[p], x[p], x[p + L.px], x[p - L.px], x[p + 1], x[p - 1], sA);
+            }
+        }
+        rs[q] = rv;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < S2_TH * S2_TW; q += blockDim.x) {
+        const int a0 = q / S2_TW, a1 = q % S2_TW;
+        const int i0 = r0 + a0, i1 = c0 + a1;
+        if (i0 >= n || i1 >= n) continue;
+        T acc = T(0);
+        const int nt = tnt<T, S>(M);
+#pragma unroll
+        for (int k = 0; k < (S == SHAPE_GENERIC ? kMaxTerms : ShapeT<(S == SHAPE_GENERIC ? 1 : S)>::nt); ++k) {
+            if (S == SHAPE_GENERIC && k >= nt) break;
+            const int o0 = toff<T, S>(M, k, 0), o1 = toff<T, S>(M, k, 1);
+            acc = O::add(acc, O::mul(M.c[k], rs[(a0 + 1 + o0) * RW + (a1 + 1 + o1)]));
+        }
+        const long long p = pidx2(L, i0, i1);
+        xo[p] = relax<T>(FZ ? T(0) : x[p], acc, sM, omega);
+    }
+}
+
+template <class T, int S, bool FZ>
+__global__ void __launch_bounds__(256) k_sweep3d_tile(Layout L, const T* __restrict__ x, const T* __restrict__ b,
+                                                      T* __restrict__ xo, Terms<T> M, T sA, T sM, T omega) {
+    using O = Op<T>;
+    constexpr int RX = S3_TX + 2, RY = S3_TY + 2, RZ = S3_TZ + 2;
+    __shared__ T rs[RZ * RY * RX];
+    const int x0 = blockIdx.x * S3_TX, y0 = blockIdx.y * S3_TY, z0 = blockIdx.z * S3_TZ;
+    const int n = L.n;
+    for (int q = threadIdx.x; q < RZ * RY * RX; q += blockDim.x) {
+        const int i0 = z0 - 1 + q / (RY * RX), i1 = y0 - 1 + (q / RX) % RY, i2 = x0 - 1 + q % RX;
+        T rv = T(0);
+        if (i0 >= 0 && i0 < n && i1 >= 0 && i1 < n && i2 >= 0 && i2 < n) {
+            const long long p = pidx3(L, i0, i1, i2);
+            if constexpr (FZ) {
+                rv = b[p];
+            } else {
+                rv = residual3d<T>(b[p], x[p], x[p + L.pp], x[p - L.pp], x[p + L.px], x[p - L.px], x[p + 1], x[p - 1],
+                                   sA);
+            }
+        }
+        rs[q] = rv;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < S3_TZ * S3_TY * S3_TX; q += blockDim.x) {
+        const int a0 = q / (S3_TY * S3_TX), a1 = (q / S3_TX) % S3_TY, a2 = q % S3_TX;
+        const int i0 = z0 + a0, i1 = y0 + a1, i2 = x0 + a2;
+        if (i0 >= n || i1 >= n || i2 >= n) continue;
+        T acc = T(0);
+        const int nt = tnt<T, S>(M);
+#pragma unroll
+        for (int k = 0; k < (S == SHAPE_GENERIC ? kMaxTerms : ShapeT<(S == SHAPE_GENERIC ? 1 : S)>::nt); ++k) {
+            if (S == SHAPE_GENERIC && k >= nt) break;
+            const int o0 = toff<T, S>(M, k, 0), o1 = toff<T, S>(M, k, 1), o2 = toff<T, S>(M, k, 2);
+            acc = O::add(acc, O::mul(M.c[k], rs[((a0 + 1 + o0) * RY + (a1 + 1 + o1)) * RX + (a2 + 1 + o2)]));
+        }
+        const long long p = pidx3(L, i0, i1, i2);
+        xo[p] = relax<T>(FZ ? T(0) : x[p], acc, sM, omega);
+    }
+}
+
+bool sweep_fused_supported(int dim, int shape) {
+    if (dim == 2) return shape == SHAPE_GENERIC || shape == SHAPE_C1 || shape == SHAPE_STAR5 || shape == SHAPE_BOX9;
+    return shape == SHAPE_GENERIC || shape == SHAPE_C1 || shape == SHAPE_STAR7;
+}
+
+template <class T, int S, bool FZ>
+static cudaError_t sweep_dispatch(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
+                                  T omega, cudaStream_t s) {
+    if (L.dim == 2) {
+        dim3 g((L.n + S2_TW - 1) / S2_TW, (L.n + S2_TH - 1) / S2_TH);
+        k_sweep2d_tile<T, S, FZ><<<g, 256, 0, s>>>(L, x, b, xo, M, sA, sM, omega);
+    } else {
+        dim3 g((L.n + S3_TX - 1) / S3_TX, (L.n + S3_TY - 1) / S3_TY, (L.n + S3_TZ - 1) / S3_TZ);
+        k_sweep3d_tile<T, S, FZ><<<g, 256, 0, s>>>(L, x, b, xo, M, sA, sM, omega);
+    }
+    return cudaGetLastError();
+}
+
+template <class T, int S>
+static cudaError_t sweep_fz(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM, T omega,
+                            bool fz, cudaStream_t s) {
+    return fz ? sweep_dispatch<T, S, true>(L, x, b, xo, M, sA, sM, omega, s)
+              : sweep_dispatch<T, S, false>(L, x, b, xo, M, sA, sM, omega, s);
+}
+
+template <class T>
+cudaError_t launch_sweep(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, int shape, T sA, T sM,
+                         T omega, bool from_zero, cudaStream_t s) {
+    switch (shape) {
+        case SHAPE_C1: return sweep_fz<T, SHAPE_C1>(L, x, b, xo, M, sA, sM, omega, from_zero, s);
+        case SHAPE_STAR5:
+            if (L.dim == 2) return sweep_fz<T, SHAPE_STAR5>(L, x, b, xo, M, sA, sM, omega, from_zero, s);
+            break;
+        case SHAPE_BOX9:
+            if (L.dim == 2) return sweep_fz<T, SHAPE_BOX9>(L, x, b, xo, M, sA, sM, omega, from_zero, s);
+            break;
+        case SHAPE_STAR7:
+            if (L.dim == 3) return sweep_fz<T, SHAPE_STAR7>(L, x, b, xo, M, sA, sM, omega, from_zero, s);
+            break;
+        default: break;
+    }
+    return sweep_fz<T, SHAPE_GENERIC>(L, x, b, xo, M, sA, sM, omega, from_zero, s);
+}
+
+// ------------------------------------------------------------------------------------------
+// K2 v1: residual into scratch, then restriction
+// ------------------------------------------------------------------------------------------
+template <class T>
+cudaError_t launch_residual_restrict(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T sA,
+                                     T* scratch_r, cudaStream_t s) {
+    cudaError_t e = launch_residual<T>(Lf, x, b, scratch_r, sA, s);
+    if (e != cudaSuccess) return e;
+    return launch_restrict<T>(Lf, Lc, scratch_r, bc, s);
+}
+
+template cudaError_t launch_sweep<double>(const Layout&, const double*, const double*, double*, const Terms<double>&,
+                                          int, double, double, double, bool, cudaStream_t);
+template cudaError_t launch_sweep<float>(const Layout&, const float*, const float*, float*, const Terms<float>&, int,
+                                         float, float, float, bool, cudaStream_t);
+template cudaError_t launch_residual_restrict<double>(const Layout&, const Layout&, const double*, const double*,
+                                                      double*, double, double*, cudaStream_t);
+template cudaError_t launch_residual_restrict<float>(const Layout&, const Layout&, const float*, const float*, float*,
+                                                     float, float*, cudaStream_t);
+
+}  // namespace spaimg

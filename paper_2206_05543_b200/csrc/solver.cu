@@ -1,0 +1,764 @@
+// C-ABI entry points (include/spaimg_cuda.h) and the native multigrid runtime: the padded
+// level hierarchy, the V/W-cycle schedule (reference multigrid.py:157-185) captured into a
+// CUDA graph, and the solve loop (multigrid.py:203-219).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "spaimg_cuda.h"
+
+using namespace spaimg;
+
+// ------------------------------------------------------------------------------------------
+// errors
+// ------------------------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(expr)                                                                                          \
+    do {                                                                                                  \
+        cudaError_t e_ = (expr);                                                                          \
+        if (e_ != cudaSuccess) return fail((int)e_, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+extern "C" const char* spaimg_last_error(void) { return g_err.c_str(); }
+extern "C" int spaimg_abi_version(void) { return SPAIMG_ABI_VERSION; }
+extern "C" int spaimg_set_device(int device) {
+    CK(cudaSetDevice(device));
+    return 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// helpers
+// ------------------------------------------------------------------------------------------
+static bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static long long count_of(int dim, int N) {
+    const long long n = N - 1;
+    return dim == 2 ? n * n : n * n * n;
+}
+
+static int stencil_radius(const spaimg_stencil& S) {
+    int w = 0;
+    for (int k = 0; k < S.nterms; ++k)
+        for (int a = 0; a < S.dim; ++a) w = std::max(w, std::abs(S.offsets[k][a]));
+    return w;
+}
+
+static bool same_offsets(const spaimg_stencil& S, int shape) {
+    auto o = [&](int k, int a) -> int {
+        switch (shape) {
+            case SHAPE_C1: return ShapeT<SHAPE_C1>::o(k, a);
+            case SHAPE_STAR5: return ShapeT<SHAPE_STAR5>::o(k, a);
+            case SHAPE_BOX9: return ShapeT<SHAPE_BOX9>::o(k, a);
+            case SHAPE_STAR7: return ShapeT<SHAPE_STAR7>::o(k, a);
+        }
+        return 99;
+    };
+    int nt = shape == SHAPE_C1 ? 1 : shape == SHAPE_STAR5 ? 5 : shape == SHAPE_BOX9 ? 9 : 7;
+    if (S.nterms != nt) return false;
+    for (int k = 0; k < nt; ++k)
+        for (int a = 0; a < S.dim; ++a)
+            if (S.offsets[k][a] != o(k, a)) return false;
+    return true;
+}
+
+static int detect_shape(const spaimg_stencil& S) {
+    if (same_offsets(S, SHAPE_C1)) return SHAPE_C1;
+    if (S.dim == 2 && same_offsets(S, SHAPE_STAR5)) return SHAPE_STAR5;
+    if (S.dim == 2 && same_offsets(S, SHAPE_BOX9)) return SHAPE_BOX9;
+    if (S.dim == 3 && same_offsets(S, SHAPE_STAR7)) return SHAPE_STAR7;
+    return SHAPE_GENERIC;
+}
+
+template <class T>
+static Terms<T> to_terms(const spaimg_stencil& S) {
+    Terms<T> t{};
+    t.nt = S.nterms;
+    for (int k = 0; k < S.nterms; ++k) {
+        for (int a = 0; a < 3; ++a) t.off[k][a] = a < S.dim ? S.offsets[k][a] : 0;
+        t.c[k] = (T)S.coef[k];
+    }
+    return t;
+}
+
+// Python evaluates the mesh scale as (1.0 / N) ** e, i.e. C pow() (stencils.py:152)
+static double hscale(int N, int e) { return std::pow(1.0 / (double)N, (double)e); }
+
+static int check_stencil(const spaimg_stencil* S, int dim) {
+    if (!S) return fail(SPAIMG_EINVAL, "stencil is NULL");
+    if (S->dim != dim) return fail(SPAIMG_EINVAL, "stencil dim does not match grid dim");
+    if (S->nterms < 1 || S->nterms > SPAIMG_MAX_TERMS) return fail(SPAIMG_EINVAL, "stencil needs 1..27 entries");
+    return 0;
+}
+
+static int check_dims(int dtype, int dim, int N) {
+    if (dtype != SPAIMG_F64 && dtype != SPAIMG_F32) return fail(SPAIMG_EINVAL, "dtype must be SPAIMG_F64 or SPAIMG_F32");
+    if (dim != 2 && dim != 3) return fail(SPAIMG_EINVAL, "dim must be 2 or 3");
+    if (N < 2) return fail(SPAIMG_EINVAL, "need N >= 2");
+    return 0;
+}
+
+// A padded level with its buffers; owns cudaMalloc'd (or stream-ordered) memory.
+template <class T> struct Level {
+    Layout L{};
+    T* x[2] = {nullptr, nullptr};
+    T* b = nullptr;
+    T* r = nullptr;  // scratch for unfused paths
+    T sA{}, sM{};
+};
+
+// Stream-ordered scratch allocations for one-shot C-ABI calls.
+struct Scratch {
+    cudaStream_t s;
+    std::vector<void*> ptrs;
+    explicit Scratch(cudaStream_t st) : s(st) {}
+    template <class T> cudaError_t get(T** p, size_t count) {
+        void* q = nullptr;
+        cudaError_t e = cudaMallocAsync(&q, count * sizeof(T), s);
+        if (e != cudaSuccess) return e;
+        ptrs.push_back(q);
+        *p = static_cast<T*>(q);
+        return cudaMemsetAsync(q, 0, count * sizeof(T), s);
+    }
+    ~Scratch() {
+        for (void* p : ptrs) cudaFreeAsync(p, s);
+    }
+};
+
+// copy a dense input (host or device) into a padded level buffer
+template <class T>
+static int load_dense(Scratch& sc, const Layout& L, const void* src, T* padded, cudaStream_t s) {
+    const long long cnt = count_of(L.dim, L.N);
+    const T* dsrc = static_cast<const T*>(src);
+    if (!is_device_ptr(src)) {
+        T* stage = nullptr;
+        CK(sc.get(&stage, (size_t)cnt));
+        CK(cudaMemcpyAsync(stage, src, (size_t)cnt * sizeof(T), cudaMemcpyHostToDevice, s));
+        dsrc = stage;
+    }
+    CK(launch_pad<T>(L, dsrc, padded, s));
+    return 0;
+}
+
+// copy a padded level buffer out to a dense destination (host or device)
+template <class T>
+static int store_dense(Scratch& sc, const Layout& L, const T* padded, void* dst, cudaStream_t s) {
+    const long long cnt = count_of(L.dim, L.N);
+    if (is_device_ptr(dst)) {
+        CK(launch_unpad<T>(L, padded, static_cast<T*>(dst), s));
+        return 0;
+    }
+    T* stage = nullptr;
+    CK(sc.get(&stage, (size_t)cnt));
+    CK(launch_unpad<T>(L, padded, stage, s));
+    CK(cudaMemcpyAsync(dst, stage, (size_t)cnt * sizeof(T), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return 0;
+}
+
+template <class T>
+static int alloc_level(Scratch& sc, Level<T>& lv, int dim, int N, bool two_x, bool with_b, bool with_r) {
+    lv.L = make_layout(dim, N, sizeof(T));
+    lv.sA = (T)hscale(N, -2);
+    CK(sc.get(&lv.x[0], (size_t)lv.L.alloc));
+    if (two_x) CK(sc.get(&lv.x[1], (size_t)lv.L.alloc));
+    if (with_b) CK(sc.get(&lv.b, (size_t)lv.L.alloc));
+    if (with_r) CK(sc.get(&lv.r, (size_t)lv.L.alloc));
+    return 0;
+}
+
+// one smoothing step on a level: x[a] -> x[1-a]
+template <class T>
+static int do_sweep(Level<T>& lv, int a, bool fz, const Terms<T>& M, int shape, bool fused, T omega, cudaStream_t s,
+                    int* launches) {
+    if (fused) {
+        CK(launch_sweep<T>(lv.L, lv.x[a], lv.b, lv.x[1 - a], M, shape, lv.sA, lv.sM, omega, fz, s));
+        if (launches) *launches += 1;
+        return 0;
+    }
+    if (fz) {
+        CK(cudaMemsetAsync(lv.x[a], 0, (size_t)lv.L.alloc * sizeof(T), s));
+        if (launches) *launches += 1;
+    }
+    CK(launch_residual<T>(lv.L, lv.x[a], lv.b, lv.r, lv.sA, s));
+    CK(launch_relax<T>(lv.L, lv.x[a], lv.r, lv.x[1 - a], M, shape, lv.sM, omega, s));
+    if (launches) *launches += 2;
+    return 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// one-shot operator entry points
+// ------------------------------------------------------------------------------------------
+template <class T>
+static int apply_t(int N, const spaimg_stencil* S, const void* x, void* out, cudaStream_t s) {
+    Scratch sc(s);
+    const int dim = S->dim;
+    const long long cnt = count_of(dim, N);
+    const T* dx = static_cast<const T*>(x);
+    T* dout = static_cast<T*>(out);
+    const bool host_out = !is_device_ptr(out);
+    if (!is_device_ptr(x)) {
+        T* st = nullptr;
+        CK(sc.get(&st, (size_t)cnt));
+        CK(cudaMemcpyAsync(st, x, (size_t)cnt * sizeof(T), cudaMemcpyHostToDevice, s));
+        dx = st;
+    }
+    if (host_out) CK(sc.get(&dout, (size_t)cnt));
+    CK(launch_apply_dense<T>(dim, N, dx, dout, to_terms<T>(*S), (T)hscale(N, S->h_exponent), s));
+    if (host_out) {
+        CK(cudaMemcpyAsync(out, dout, (size_t)cnt * sizeof(T), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    return 0;
+}
+
+extern "C" int spaimg_apply(int dtype, int N, const spaimg_stencil* S, const void* x, void* out, void* stream) {
+    if (!S) return fail(SPAIMG_EINVAL, "stencil is NULL");
+    if (int rc = check_dims(dtype, S->dim, N)) return rc;
+    if (int rc = check_stencil(S, S->dim)) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    return dtype == SPAIMG_F64 ? apply_t<double>(N, S, x, out, s) : apply_t<float>(N, S, x, out, s);
+}
+
+template <class T>
+static int smooth_t(int dim, int N, const void* u, const void* b, const spaimg_stencil* Ms, double omega, int steps,
+                    void* out, cudaStream_t s) {
+    Scratch sc(s);
+    Level<T> lv;
+    const int rad = stencil_radius(*Ms);
+    const int shape = detect_shape(*Ms);
+    const bool fused = rad <= 1 && sweep_fused_supported(dim, shape);
+    if (int rc = alloc_level<T>(sc, lv, dim, N, true, true, !fused)) return rc;
+    lv.sM = (T)hscale(N, Ms->h_exponent);
+    if (int rc = load_dense<T>(sc, lv.L, u, lv.x[0], s)) return rc;
+    if (steps > 0)
+        if (int rc = load_dense<T>(sc, lv.L, b, lv.b, s)) return rc;
+    const Terms<T> M = to_terms<T>(*Ms);
+    int a = 0;
+    for (int k = 0; k < steps; ++k) {
+        if (int rc = do_sweep<T>(lv, a, false, M, shape, fused, (T)omega, s, nullptr)) return rc;
+        a = 1 - a;
+    }
+    return store_dense<T>(sc, lv.L, lv.x[a], out, s);
+}
+
+extern "C" int spaimg_smooth(int dtype, int dim, int N, const void* u, const void* b, const spaimg_stencil* M,
+                             double omega, int steps, void* out, void* stream) {
+    if (int rc = check_dims(dtype, dim, N)) return rc;
+    if (int rc = check_stencil(M, dim)) return rc;
+    if (steps < 0) return fail(SPAIMG_EINVAL, "steps must be non-negative");
+    if (stencil_radius(*M) > kGhost) return fail(SPAIMG_ENOTSUP, "smoother stencil radius > 2 is not supported");
+    cudaStream_t s = (cudaStream_t)stream;
+    return dtype == SPAIMG_F64 ? smooth_t<double>(dim, N, u, b, M, omega, steps, out, s)
+                               : smooth_t<float>(dim, N, u, b, M, omega, steps, out, s);
+}
+
+static int check_halving(int N) {
+    if (N % 2) return fail(SPAIMG_EINVAL, "cannot halve an odd mesh count N=" + std::to_string(N));
+    if (N / 2 < 2) return fail(SPAIMG_EINVAL, "coarse mesh would have no interior points");
+    return 0;
+}
+
+template <class T>
+static int restrict_t(int dim, int N, const void* fine, void* coarse, cudaStream_t s) {
+    Scratch sc(s);
+    Level<T> f, c;
+    if (int rc = alloc_level<T>(sc, f, dim, N, false, false, false)) return rc;
+    if (int rc = alloc_level<T>(sc, c, dim, N / 2, false, false, false)) return rc;
+    if (int rc = load_dense<T>(sc, f.L, fine, f.x[0], s)) return rc;
+    CK(launch_restrict<T>(f.L, c.L, f.x[0], c.x[0], s));
+    return store_dense<T>(sc, c.L, c.x[0], coarse, s);
+}
+
+extern "C" int spaimg_restrict(int dtype, int dim, int N, const void* fine, void* coarse, void* stream) {
+    if (int rc = check_dims(dtype, dim, N)) return rc;
+    if (int rc = check_halving(N)) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    return dtype == SPAIMG_F64 ? restrict_t<double>(dim, N, fine, coarse, s) : restrict_t<float>(dim, N, fine, coarse, s);
+}
+
+template <class T>
+static int prolong_t(int dim, int Nc, const void* coarse, const void* base, void* fine, cudaStream_t s) {
+    Scratch sc(s);
+    Level<T> f, c;
+    if (int rc = alloc_level<T>(sc, f, dim, 2 * Nc, false, false, false)) return rc;
+    if (int rc = alloc_level<T>(sc, c, dim, Nc, false, false, false)) return rc;
+    if (int rc = load_dense<T>(sc, c.L, coarse, c.x[0], s)) return rc;
+    if (base)
+        if (int rc = load_dense<T>(sc, f.L, base, f.x[0], s)) return rc;
+    // prolong(e) alone stores the interpolant (multigrid.py:125-129); with a base grid it is
+    // the correction u + prolong(e) of multigrid.py:184.
+    CK(launch_prolong_correct<T>(f.L, c.L, f.x[0], c.x[0], s, base != nullptr));
+    return store_dense<T>(sc, f.L, f.x[0], fine, s);
+}
+
+extern "C" int spaimg_prolong(int dtype, int dim, int coarse_N, const void* coarse, void* fine, void* stream) {
+    if (int rc = check_dims(dtype, dim, coarse_N)) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    return dtype == SPAIMG_F64 ? prolong_t<double>(dim, coarse_N, coarse, nullptr, fine, s)
+                               : prolong_t<float>(dim, coarse_N, coarse, nullptr, fine, s);
+}
+
+extern "C" int spaimg_prolong_correct(int dtype, int dim, int N, const void* u, const void* e, void* out, void* stream) {
+    if (int rc = check_dims(dtype, dim, N)) return rc;
+    if (int rc = check_halving(N)) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    return dtype == SPAIMG_F64 ? prolong_t<double>(dim, N / 2, e, u, out, s)
+                               : prolong_t<float>(dim, N / 2, e, u, out, s);
+}
+
+template <class T>
+static int residual_restrict_t(int dim, int N, const void* u, const void* b, void* coarse, cudaStream_t s) {
+    Scratch sc(s);
+    Level<T> f, c;
+    if (int rc = alloc_level<T>(sc, f, dim, N, false, true, true)) return rc;
+    if (int rc = alloc_level<T>(sc, c, dim, N / 2, false, false, false)) return rc;
+    if (int rc = load_dense<T>(sc, f.L, u, f.x[0], s)) return rc;
+    if (int rc = load_dense<T>(sc, f.L, b, f.b, s)) return rc;
+    CK(launch_residual_restrict<T>(f.L, c.L, f.x[0], f.b, c.x[0], f.sA, f.r, s));
+    return store_dense<T>(sc, c.L, c.x[0], coarse, s);
+}
+
+extern "C" int spaimg_residual_restrict(int dtype, int dim, int N, const void* u, const void* b, void* coarse,
+                                        void* stream) {
+    if (int rc = check_dims(dtype, dim, N)) return rc;
+    if (int rc = check_halving(N)) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    return dtype == SPAIMG_F64 ? residual_restrict_t<double>(dim, N, u, b, coarse, s)
+                               : residual_restrict_t<float>(dim, N, u, b, coarse, s);
+}
+
+template <class T>
+static int norm_t(int dim, int N, const void* u, const void* b, double* out, cudaStream_t s) {
+    Scratch sc(s);
+    Level<T> f;
+    if (int rc = alloc_level<T>(sc, f, dim, N, false, true, false)) return rc;
+    if (int rc = load_dense<T>(sc, f.L, u, f.x[0], s)) return rc;
+    if (int rc = load_dense<T>(sc, f.L, b, f.b, s)) return rc;
+    double* part = nullptr;
+    double* nrm = nullptr;
+    unsigned* cnt = nullptr;
+    CK(sc.get(&part, kNormBlocks));
+    CK(sc.get(&nrm, 1));
+    CK(sc.get(&cnt, 1));
+    CK(launch_residual_norm<T>(f.L, f.x[0], f.b, f.sA, part, cnt, nrm, 0, nullptr, s));
+    CK(cudaMemcpyAsync(out, nrm, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return 0;
+}
+
+extern "C" int spaimg_residual_norm(int dtype, int dim, int N, const void* u, const void* b, double* out, void* stream) {
+    if (int rc = check_dims(dtype, dim, N)) return rc;
+    if (!out) return fail(SPAIMG_EINVAL, "out is NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    return dtype == SPAIMG_F64 ? norm_t<double>(dim, N, u, b, out, s) : norm_t<float>(dim, N, u, b, out, s);
+}
+
+// ------------------------------------------------------------------------------------------
+// the solver: level hierarchy + captured cycle
+// ------------------------------------------------------------------------------------------
+struct spaimg_solver {
+    virtual ~spaimg_solver() = default;
+    virtual int load(const void* b, const void* u0, cudaStream_t s) = 0;
+    virtual int cycles(int n, cudaStream_t s) = 0;
+    virtual int run(double tol, int max_iters, double* norms, int* iters, int* conv, cudaStream_t s) = 0;
+    virtual int store(void* out, cudaStream_t s) = 0;
+    virtual int op(int which, int reps, cudaStream_t s) = 0;
+    virtual void stats(spaimg_solver_stats* st) const = 0;
+};
+
+template <class T> struct Solver final : spaimg_solver {
+    spaimg_mg_config cfg{};
+    std::vector<double> lu_h;
+    std::vector<int> piv_h;
+    std::vector<Level<T>> lv;  // lv[0] finest ... lv.back() = coarse-solve level
+    Terms<T> M{};
+    int shape = SHAPE_GENERIC;
+    bool fused = false;
+    T omega{};
+    T* lu = nullptr;
+    int* piv = nullptr;
+    int nlu = 0;
+    double* norms_d = nullptr;
+    int norms_cap = 0;
+    int* slot_d = nullptr;
+    double* partials = nullptr;
+    unsigned* counter = nullptr;
+    double* norms_h = nullptr;  // pinned
+    T* stage = nullptr;         // dense staging on device
+    int cur = 0;                // buffer of lv[0] holding the iterate
+    cudaGraphExec_t exec[2] = {nullptr, nullptr};
+    int kernels_per_cycle = 0;
+    bool use_graph = true;
+    std::vector<void*> owned;
+
+    ~Solver() override {
+        for (int i = 0; i < 2; ++i)
+            if (exec[i]) cudaGraphExecDestroy(exec[i]);
+        for (void* p : owned) cudaFree(p);
+        if (norms_h) cudaFreeHost(norms_h);
+    }
+
+    template <class U> int dalloc(U** p, size_t count) {
+        void* q = nullptr;
+        CK(cudaMalloc(&q, count * sizeof(U) > 0 ? count * sizeof(U) : 16));
+        owned.push_back(q);
+        CK(cudaMemset(q, 0, count * sizeof(U)));
+        *p = static_cast<U*>(q);
+        return 0;
+    }
+
+    int init(const spaimg_mg_config& c) {
+        cfg = c;
+        lu_h.assign(c.coarse_lu, c.coarse_lu + (size_t)c.coarse_n * c.coarse_n);
+        piv_h.assign(c.coarse_piv, c.coarse_piv + c.coarse_n);
+        cfg.coarse_lu = nullptr;
+        cfg.coarse_piv = nullptr;
+        const char* eg = getenv("SPAIMG_NO_GRAPH");
+        use_graph = !(eg && eg[0] == '1');
+        M = to_terms<T>(c.M);
+        shape = detect_shape(c.M);
+        fused = stencil_radius(c.M) <= 1 && sweep_fused_supported(c.dim, shape);
+        omega = (T)c.omega;
+        // levels: halve until N <= coarsest_N (multigrid.py:166, :178)
+        int N = c.N;
+        while (true) {
+            Level<T> l;
+            l.L = make_layout(c.dim, N, sizeof(T));
+            l.sA = (T)hscale(N, -2);
+            l.sM = (T)hscale(N, c.M.h_exponent);
+            const bool coarse = N <= c.coarsest_N;
+            if (int rc = dalloc(&l.x[0], (size_t)l.L.alloc)) return rc;
+            if (int rc = dalloc(&l.b, (size_t)l.L.alloc)) return rc;
+            if (!coarse) {
+                if (int rc = dalloc(&l.x[1], (size_t)l.L.alloc)) return rc;
+                if (int rc = dalloc(&l.r, (size_t)l.L.alloc)) return rc;
+            }
+            lv.push_back(l);
+            if (coarse) break;
+            if (N % 2) return fail(SPAIMG_EINVAL, "cannot halve an odd mesh count N=" + std::to_string(N));
+            if (N / 2 < 2) return fail(SPAIMG_EINVAL, "coarse mesh would have no interior points");
+            N /= 2;
+        }
+        if (N != c.coarse_N || count_of(c.dim, N) != c.coarse_n)
+            return fail(SPAIMG_EINVAL, "coarse factorisation does not match the coarsest level");
+        nlu = c.coarse_n;
+        std::vector<T> luT(lu_h.begin(), lu_h.end());
+        if (int rc = dalloc(&lu, luT.size())) return rc;
+        CK(cudaMemcpy(lu, luT.data(), luT.size() * sizeof(T), cudaMemcpyHostToDevice));
+        if (int rc = dalloc(&piv, piv_h.size())) return rc;
+        CK(cudaMemcpy(piv, piv_h.data(), piv_h.size() * sizeof(int), cudaMemcpyHostToDevice));
+        norms_cap = 4097;
+        if (int rc = dalloc(&norms_d, norms_cap)) return rc;
+        if (int rc = dalloc(&slot_d, 1)) return rc;
+        if (int rc = dalloc(&partials, kNormBlocks)) return rc;
+        if (int rc = dalloc(&counter, 1)) return rc;
+        if (int rc = dalloc(&stage, (size_t)count_of(c.dim, c.N))) return rc;
+        CK(cudaMallocHost(&norms_h, sizeof(double) * norms_cap));
+        return 0;
+    }
+
+    int nsmooth() const { return (int)lv.size() - 1; }
+
+    // recursive schedule (multigrid.py:157-185).  Returns the buffer index of level l holding
+    // the result, or -1 on error.
+    int visit(int l, int a, bool fz, cudaStream_t s, int* launches) {
+        Level<T>& L = lv[l];
+        if (l == nsmooth()) {  // u.N <= coarsest_N: direct solve (multigrid.py:166-167)
+            if (launch_coarse_solve<T>(L.L, L.b, L.x[0], lu, piv, nlu, s) != cudaSuccess) return -1;
+            ++*launches;
+            return 0;
+        }
+        for (int k = 0; k < cfg.nu1; ++k) {
+            if (do_sweep<T>(L, a, fz, M, shape, fused, omega, s, launches)) return -1;
+            a = 1 - a;
+            fz = false;
+        }
+        if (fz) {  // nu1 == 0 on a zero start: materialise the zero iterate
+            if (cudaMemsetAsync(L.x[a], 0, (size_t)L.L.alloc * sizeof(T), s) != cudaSuccess) return -1;
+            ++*launches;
+        }
+        Level<T>& C = lv[l + 1];
+        if (launch_residual_restrict<T>(L.L, C.L, L.x[a], L.b, C.b, L.sA, L.r, s) != cudaSuccess) return -1;
+        *launches += 2;
+        int c;
+        if (l + 1 == nsmooth()) {
+            if (launch_coarse_solve<T>(C.L, C.b, C.x[0], lu, piv, nlu, s) != cudaSuccess) return -1;
+            ++*launches;
+            c = 0;
+        } else {
+            c = visit(l + 1, 0, true, s, launches);
+            for (int g = 1; g < cfg.gamma && c >= 0; ++g) c = visit(l + 1, c, false, s, launches);
+            if (c < 0) return -1;
+        }
+        if (launch_prolong_correct<T>(L.L, C.L, L.x[a], C.x[c], s) != cudaSuccess) return -1;
+        ++*launches;
+        for (int k = 0; k < cfg.nu2; ++k) {
+            if (do_sweep<T>(L, a, false, M, shape, fused, omega, s, launches)) return -1;
+            a = 1 - a;
+        }
+        return a;
+    }
+
+    int norm_into_history(int a, cudaStream_t s) {
+        CK(launch_residual_norm<T>(lv[0].L, lv[0].x[a], lv[0].b, lv[0].sA, partials, counter, norms_d, 0, slot_d, s));
+        return 0;
+    }
+
+    // one cycle + its residual norm, starting from lv[0].x[a]; returns the final buffer
+    int cycle_body(int a, cudaStream_t s, int* launches) {
+        const int out = visit(0, a, false, s, launches);
+        if (out < 0) return -1;
+        if (nsmooth() == 0) {
+            // single-level problem: the cycle IS the direct solve into x[0]
+        }
+        if (norm_into_history(out, s)) return -1;
+        ++*launches;
+        return out;
+    }
+
+    int build_graph(int a) {
+        cudaStream_t cs;
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        cudaGraph_t g;
+        cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) {
+            cudaStreamDestroy(cs);
+            return fail((int)e, std::string("begin capture: ") + cudaGetErrorString(e));
+        }
+        int launches = 0;
+        const int out = cycle_body(a, cs, &launches);
+        e = cudaStreamEndCapture(cs, &g);
+        cudaStreamDestroy(cs);
+        if (out < 0) {
+            if (e == cudaSuccess) cudaGraphDestroy(g);
+            return fail(SPAIMG_EINVAL, "cycle capture failed: " + g_err);
+        }
+        if (e != cudaSuccess) return fail((int)e, std::string("end capture: ") + cudaGetErrorString(e));
+        e = cudaGraphInstantiate(&exec[a], g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail((int)e, std::string("graph instantiate: ") + cudaGetErrorString(e));
+        kernels_per_cycle = launches;
+        return 0;
+    }
+
+    int final_buffer(int a) const {
+        if (nsmooth() == 0) return 0;
+        return (cfg.nu1 + cfg.nu2) % 2 ? 1 - a : a;
+    }
+
+    int one_cycle(cudaStream_t s) {
+        if (use_graph) {
+            if (!exec[cur])
+                if (int rc = build_graph(cur)) return rc;
+            CK(cudaGraphLaunch(exec[cur], s));
+            cur = final_buffer(cur);
+            return 0;
+        }
+        int launches = 0;
+        const int out = cycle_body(cur, s, &launches);
+        if (out < 0) return fail(SPAIMG_EINVAL, "cycle failed: " + g_err);
+        kernels_per_cycle = launches;
+        cur = out;
+        return 0;
+    }
+
+    int load(const void* b, const void* u0, cudaStream_t s) override {
+        Scratch sc(s);
+        Level<T>& L = lv[0];
+        if (b)  // NULL keeps the right-hand side already loaded
+            if (int rc = load_dense<T>(sc, L.L, b, L.b, s)) return rc;
+        cur = 0;
+        if (u0) {
+            if (int rc = load_dense<T>(sc, L.L, u0, L.x[0], s)) return rc;
+        } else {
+            CK(cudaMemsetAsync(L.x[0], 0, (size_t)L.L.alloc * sizeof(T), s));
+        }
+        CK(cudaMemsetAsync(slot_d, 0, sizeof(int), s));
+        return 0;
+    }
+
+    int cycles(int n, cudaStream_t s) override {
+        for (int k = 0; k < n; ++k)
+            if (int rc = one_cycle(s)) return rc;
+        return 0;
+    }
+
+    int run(double tol, int max_iters, double* norms, int* iters, int* conv, cudaStream_t s) override {
+        if (max_iters + 1 > norms_cap) return fail(SPAIMG_EINVAL, "max_iters too large");
+        CK(cudaMemsetAsync(slot_d, 0, sizeof(int), s));
+        if (int rc = norm_into_history(cur, s)) return rc;
+        CK(cudaMemcpyAsync(norms_h, norms_d, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        norms[0] = norms_h[0];
+        int k = 0;
+        *conv = 0;
+        while (k < max_iters) {
+            if (int rc = one_cycle(s)) return rc;
+            ++k;
+            CK(cudaMemcpyAsync(norms_h + k, norms_d + k, sizeof(double), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            norms[k] = norms_h[k];
+            if (norms[k] <= tol * norms[0]) {
+                *conv = 1;
+                break;
+            }
+        }
+        *iters = k;
+        return 0;
+    }
+
+    int store(void* out, cudaStream_t s) override {
+        Scratch sc(s);
+        return store_dense<T>(sc, lv[0].L, lv[0].x[cur], out, s);
+    }
+
+    int op(int which, int reps, cudaStream_t s) override {
+        Level<T>& L = lv[0];
+        for (int k = 0; k < reps; ++k) {
+            switch (which) {
+                case 0:
+                    if (nsmooth() < 1) return fail(SPAIMG_EINVAL, "no smoothing level");
+                    if (int rc = do_sweep<T>(L, cur, false, M, shape, fused, omega, s, nullptr)) return rc;
+                    break;
+                case 1:
+                    if (nsmooth() < 1) return fail(SPAIMG_EINVAL, "no coarse level");
+                    CK(launch_residual_restrict<T>(L.L, lv[1].L, L.x[cur], L.b, lv[1].b, L.sA, L.r, s));
+                    break;
+                case 2:
+                    if (nsmooth() < 1) return fail(SPAIMG_EINVAL, "no coarse level");
+                    CK(launch_prolong_correct<T>(L.L, lv[1].L, L.x[1 - cur], lv[1].x[0], s));
+                    break;
+                case 3:
+                    CK(launch_residual_norm<T>(L.L, L.x[cur], L.b, L.sA, partials, counter, norms_d, 0, nullptr, s));
+                    break;
+                default: return fail(SPAIMG_EINVAL, "unknown op");
+            }
+        }
+        return 0;
+    }
+
+    void stats(spaimg_solver_stats* st) const override {
+        st->levels = nsmooth();
+        st->kernels_per_cycle = kernels_per_cycle;
+        st->unknowns = count_of(cfg.dim, cfg.N);
+        st->graph = use_graph ? 1 : 0;
+        st->fused_sweep = fused ? 1 : 0;
+        // per visit of level l: n_l s (3(nu1+nu2) + 4 + 2^(1-d)); + 2 s n_0 (norm)
+        const double sz = sizeof(T);
+        double bytes = 2.0 * sz * (double)count_of(cfg.dim, cfg.N);
+        double visits = 1.0;
+        for (int l = 0; l < nsmooth(); ++l) {
+            const double nl = (double)count_of(cfg.dim, lv[l].L.N);
+            bytes += visits * nl * sz * (3.0 * (cfg.nu1 + cfg.nu2) + 4.0 + std::pow(2.0, 1 - cfg.dim));
+            visits *= cfg.gamma;
+        }
+        st->bytes_per_cycle = bytes;
+    }
+};
+
+static int check_cfg(const spaimg_mg_config* c) {
+    if (!c) return fail(SPAIMG_EINVAL, "config is NULL");
+    if (int rc = check_dims(c->dtype, c->dim, c->N)) return rc;
+    if (int rc = check_stencil(&c->M, c->dim)) return rc;
+    if (c->gamma != 1 && c->gamma != 2) return fail(SPAIMG_EINVAL, "gamma must be 1 (V) or 2 (W)");
+    if (c->nu1 < 0 || c->nu2 < 0 || c->nu1 + c->nu2 < 1) return fail(SPAIMG_EINVAL, "need nu1, nu2 >= 0 with nu1 + nu2 >= 1");
+    if (c->coarsest_N < 2) return fail(SPAIMG_EINVAL, "coarsest_N must be at least 2");
+    if (stencil_radius(c->M) > kGhost) return fail(SPAIMG_ENOTSUP, "smoother stencil radius > 2 is not supported");
+    if (!c->coarse_lu || !c->coarse_piv || c->coarse_n < 1) return fail(SPAIMG_EINVAL, "missing coarse factorisation");
+    return 0;
+}
+
+extern "C" int spaimg_solver_create(const spaimg_mg_config* cfg, spaimg_solver** out) {
+    if (int rc = check_cfg(cfg)) return rc;
+    if (!out) return fail(SPAIMG_EINVAL, "out is NULL");
+    std::unique_ptr<spaimg_solver> s;
+    int rc;
+    if (cfg->dtype == SPAIMG_F64) {
+        auto p = std::make_unique<Solver<double>>();
+        rc = p->init(*cfg);
+        s = std::move(p);
+    } else {
+        auto p = std::make_unique<Solver<float>>();
+        rc = p->init(*cfg);
+        s = std::move(p);
+    }
+    if (rc) return rc;
+    *out = s.release();
+    return 0;
+}
+
+extern "C" int spaimg_solver_destroy(spaimg_solver* s) {
+    delete s;
+    return 0;
+}
+
+extern "C" int spaimg_solver_stats_get(const spaimg_solver* s, spaimg_solver_stats* st) {
+    if (!s || !st) return fail(SPAIMG_EINVAL, "NULL argument");
+    s->stats(st);
+    return 0;
+}
+
+extern "C" int spaimg_solver_load(spaimg_solver* s, const void* b, const void* u0, void* stream) {
+    if (!s) return fail(SPAIMG_EINVAL, "NULL solver");
+    return s->load(b, u0, (cudaStream_t)stream);
+}
+
+extern "C" int spaimg_solver_cycles(spaimg_solver* s, int ncycles, void* stream) {
+    if (!s) return fail(SPAIMG_EINVAL, "NULL solver");
+    return s->cycles(ncycles, (cudaStream_t)stream);
+}
+
+extern "C" int spaimg_solver_run(spaimg_solver* s, double tol, int max_iters, double* norms, int* iterations,
+                                 int* converged, void* stream) {
+    if (!s || !norms || !iterations || !converged) return fail(SPAIMG_EINVAL, "NULL argument");
+    if (max_iters < 0) return fail(SPAIMG_EINVAL, "max_iters must be non-negative");
+    return s->run(tol, max_iters, norms, iterations, converged, (cudaStream_t)stream);
+}
+
+extern "C" int spaimg_solver_store(spaimg_solver* s, void* u_out, void* stream) {
+    if (!s || !u_out) return fail(SPAIMG_EINVAL, "NULL argument");
+    return s->store(u_out, (cudaStream_t)stream);
+}
+
+extern "C" int spaimg_solver_op(spaimg_solver* s, int op, int reps, void* stream) {
+    if (!s) return fail(SPAIMG_EINVAL, "NULL solver");
+    return s->op(op, reps, (cudaStream_t)stream);
+}
+
+extern "C" int spaimg_cycle(const spaimg_mg_config* cfg, const void* u, const void* b, void* out, void* stream) {
+    spaimg_solver* s = nullptr;
+    if (int rc = spaimg_solver_create(cfg, &s)) return rc;
+    std::unique_ptr<spaimg_solver> own(s);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (int rc = s->load(b, u, st)) return rc;
+    if (int rc = s->cycles(1, st)) return rc;
+    return s->store(out, st);
+}
+
+extern "C" int spaimg_solve(const spaimg_mg_config* cfg, const void* b, const void* u0, void* u_out, double tol,
+                            int max_iters, double* norms, int* iterations, int* converged, void* stream) {
+    spaimg_solver* s = nullptr;
+    if (int rc = spaimg_solver_create(cfg, &s)) return rc;
+    std::unique_ptr<spaimg_solver> own(s);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (int rc = s->load(b, u0, st)) return rc;
+    if (int rc = s->run(tol, max_iters, norms, iterations, converged, st)) return rc;
+    return s->store(u_out, st);
+}

@@ -1,0 +1,478 @@
+"""GPU drop-in for the reference `spaimg.multigrid` API
+(reference pkg/src/spaimg/multigrid.py:19-227).
+
+Same names, signatures, defaults, exceptions and return types as the
+reference; the work runs in hand-written sm_100a kernels behind the C ABI of
+include/spaimg_cuda.h (loaded by `_lib`).  Host (numpy) inputs give host
+outputs, CUDA-tensor inputs give CUDA-tensor outputs.  There is no CPU path.
+
+Extensions over the reference (all optional, defaults reproduce it):
+  * `solve(b, cfg, u0=None)`: u0=None draws the reference's seeded U(0,1) start
+    (multigrid.py:204-205) on the host; pass an array/Grid (or 0) to start elsewhere.
+  * float32 device grids (torch float32 tensors) run the fp32 kernels.
+"""
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .grids import Grid, is_device_array
+from .stencils import NamedSmoother, Stencil, laplacian
+
+__all__ = [
+    "MgConfig",
+    "SolveReport",
+    "smooth",
+    "restrict",
+    "prolong",
+    "cycle",
+    "solve",
+    "Solver",
+]
+
+
+# ------------------------------------------------------------------------------------------
+# configuration and report (multigrid.py:30-83)
+# ------------------------------------------------------------------------------------------
+def _is_named(sm) -> bool:
+    return isinstance(sm, NamedSmoother) or (
+        hasattr(sm, "stencil") and hasattr(sm, "omega_opt_analytic"))
+
+
+def _is_stencil(sm) -> bool:
+    return isinstance(sm, Stencil) or (
+        hasattr(sm, "entries") and hasattr(sm, "h_exponent") and hasattr(sm, "dim"))
+
+
+@dataclass
+class MgConfig:
+    """Multigrid cycle configuration (reference multigrid.py:30-68), same defaults."""
+
+    smoother: object
+    cycle: str = "W"
+    nu1: int = 1
+    nu2: int = 0
+    omega: float | None = None
+    coarsest_N: int = 4
+    tol: float = 1e-10
+    max_iters: int = 100
+    rng_seed: int = 0
+
+    def __post_init__(self):
+        self.cycle = self.cycle.upper()
+        if self.cycle not in ("V", "W"):
+            raise ValueError(f"cycle must be 'V' or 'W', got {self.cycle!r}")
+        if self.nu1 < 0 or self.nu2 < 0 or self.nu1 + self.nu2 < 1:
+            raise ValueError("need nu1, nu2 >= 0 with nu1 + nu2 >= 1")
+        if self.coarsest_N < 2:
+            raise ValueError("coarsest_N must be at least 2")
+        if self.tol <= 0:
+            raise ValueError("tol must be positive")
+
+    def resolve_smoother(self) -> tuple:
+        """(stencil, omega) actually used by the cycles."""
+        if _is_named(self.smoother):
+            om = self.omega if self.omega is not None else self.smoother.omega_opt_analytic
+            return self.smoother.stencil, float(om)
+        if _is_stencil(self.smoother):
+            if self.omega is None:
+                raise ValueError("a custom stencil smoother needs an explicit omega")
+            return self.smoother, float(self.omega)
+        raise TypeError(f"smoother must be NamedSmoother or Stencil, got {type(self.smoother)}")
+
+
+@dataclass
+class SolveReport:
+    """Iteration record of one multigrid solve (reference multigrid.py:71-83)."""
+
+    iterations: int
+    residual_norms: list
+    rho_hat: float
+    converged: bool
+    wall_time: float
+    error_inf: float | None = None
+
+    def __post_init__(self):
+        self.residual_norms = [float(r) for r in self.residual_norms]
+
+
+# ------------------------------------------------------------------------------------------
+# marshalling
+# ------------------------------------------------------------------------------------------
+def _stencil_struct(S) -> _lib.SpaimgStencil:
+    st = _lib.SpaimgStencil()
+    items = list(S.entries.items())
+    if len(items) > _lib.MAX_TERMS:
+        raise ValueError(f"stencil has {len(items)} entries; at most {_lib.MAX_TERMS} are supported")
+    st.dim = int(S.dim)
+    st.nterms = len(items)
+    st.h_exponent = int(S.h_exponent)
+    for k, (off, c) in enumerate(items):
+        for a in range(3):
+            st.offsets[k][a] = int(off[a]) if a < len(off) else 0
+        st.coef[k] = float(c)  # reference stencils.py:151
+    return st
+
+
+class _Arr:
+    """A grid's values as a raw pointer for the C ABI (keeps the owner alive)."""
+
+    def __init__(self, values, dtype_code):
+        self.owner = values
+        if is_device_array(values):
+            self.ptr = values.data_ptr()
+        else:
+            a = np.ascontiguousarray(values, dtype=np.float64 if dtype_code == _lib.F64 else np.float32)
+            self.owner = a
+            self.ptr = a.ctypes.data
+
+
+def _dtype_code(values) -> int:
+    if is_device_array(values):
+        import torch
+        return _lib.F32 if values.dtype == torch.float32 else _lib.F64
+    return _lib.F64
+
+
+def _stream_for(values):
+    if is_device_array(values):
+        import torch
+        _lib.check(_lib.load().spaimg_set_device(values.device.index or 0))
+        return ctypes.c_void_p(torch.cuda.current_stream(values.device).cuda_stream)
+    _lib.load()
+    return ctypes.c_void_p(0)
+
+
+def _empty_like(values, shape):
+    if is_device_array(values):
+        import torch
+        return torch.empty(shape, dtype=values.dtype, device=values.device)
+    return np.empty(shape, dtype=np.float64)
+
+
+def _same_side(ref, values):
+    """Return `values` on the same side (host/device, dtype) as `ref`."""
+    if is_device_array(ref):
+        import torch
+        if is_device_array(values):
+            return values.to(device=ref.device, dtype=ref.dtype).contiguous()
+        return torch.as_tensor(np.asarray(values, dtype=np.float64)).to(
+            device=ref.device, dtype=ref.dtype).contiguous()
+    if is_device_array(values):
+        return values.detach().cpu().numpy().astype(np.float64)
+    return np.ascontiguousarray(values, dtype=np.float64)
+
+
+# ------------------------------------------------------------------------------------------
+# hot-path API
+# ------------------------------------------------------------------------------------------
+def apply_stencil(S, u: Grid) -> Grid:
+    """Stencil.apply on the GPU (reference stencils.py:136-153)."""
+    if S.dim != u.dim:
+        raise ValueError(f"stencil dim {S.dim} != grid dim {u.dim}")
+    lib = _lib.load()
+    code = _dtype_code(u.values)
+    stream = _stream_for(u.values)
+    x = _Arr(u.values, code)
+    out = _empty_like(u.values, tuple(u.values.shape))
+    o = _Arr(out, code)
+    st = _stencil_struct(S)
+    _lib.check(lib.spaimg_apply(code, u.N, ctypes.byref(st), x.ptr, o.ptr, stream))
+    return Grid(u.N, out)
+
+
+def smooth(u: Grid, b: Grid, M, omega: float, steps: int) -> Grid:
+    """`steps` damped Richardson sweeps u <- u + omega*M*(b - A*u) (multigrid.py:86-101)."""
+    if u.N != b.N or u.dim != b.dim:
+        raise ValueError("u and b must live on the same grid")
+    if steps < 0:
+        raise ValueError("steps must be non-negative")
+    if M.dim != u.dim:
+        raise ValueError(f"stencil dim {M.dim} != grid dim {u.dim}")
+    lib = _lib.load()
+    code = _dtype_code(u.values)
+    stream = _stream_for(u.values)
+    x = _Arr(u.values, code)
+    bb = _Arr(_same_side(u.values, b.values), code)
+    out = _empty_like(u.values, tuple(u.values.shape))
+    o = _Arr(out, code)
+    st = _stencil_struct(M)
+    _lib.check(lib.spaimg_smooth(code, u.dim, u.N, x.ptr, bb.ptr, ctypes.byref(st), float(omega), int(steps),
+                                 o.ptr, stream))
+    return Grid(u.N, out)
+
+
+def restrict(fine: Grid) -> Grid:
+    """Full-weighting restriction to the mesh with half the resolution (multigrid.py:110-119)."""
+    if fine.N % 2:
+        raise ValueError(f"cannot halve an odd mesh count N={fine.N}")
+    if fine.N // 2 < 2:
+        raise ValueError("coarse mesh would have no interior points")
+    lib = _lib.load()
+    code = _dtype_code(fine.values)
+    stream = _stream_for(fine.values)
+    x = _Arr(fine.values, code)
+    Nc = fine.N // 2
+    out = _empty_like(fine.values, (Nc - 1,) * fine.dim)
+    o = _Arr(out, code)
+    _lib.check(lib.spaimg_restrict(code, fine.dim, fine.N, x.ptr, o.ptr, stream))
+    return Grid(Nc, out)
+
+
+def prolong(coarse: Grid, fine_N: int) -> Grid:
+    """d-linear interpolation to the mesh with twice the resolution (multigrid.py:133-144)."""
+    if fine_N != 2 * coarse.N:
+        raise ValueError(f"fine_N must be 2*{coarse.N}, got {fine_N}")
+    lib = _lib.load()
+    code = _dtype_code(coarse.values)
+    stream = _stream_for(coarse.values)
+    e = _Arr(coarse.values, code)
+    out = _empty_like(coarse.values, (fine_N - 1,) * coarse.dim)
+    o = _Arr(out, code)
+    _lib.check(lib.spaimg_prolong(code, coarse.dim, coarse.N, e.ptr, o.ptr, stream))
+    return Grid(fine_N, out)
+
+
+def residual_restrict(u: Grid, b: Grid) -> Grid:
+    """restrict(b - A u) in one fused launch (multigrid.py:176-177)."""
+    if u.N != b.N or u.dim != b.dim:
+        raise ValueError("u and b must live on the same grid")
+    if u.N % 2:
+        raise ValueError(f"cannot halve an odd mesh count N={u.N}")
+    if u.N // 2 < 2:
+        raise ValueError("coarse mesh would have no interior points")
+    lib = _lib.load()
+    code = _dtype_code(u.values)
+    stream = _stream_for(u.values)
+    x = _Arr(u.values, code)
+    bb = _Arr(_same_side(u.values, b.values), code)
+    Nc = u.N // 2
+    out = _empty_like(u.values, (Nc - 1,) * u.dim)
+    o = _Arr(out, code)
+    _lib.check(lib.spaimg_residual_restrict(code, u.dim, u.N, x.ptr, bb.ptr, o.ptr, stream))
+    return Grid(Nc, out)
+
+
+def prolong_correct(u: Grid, e: Grid) -> Grid:
+    """u + prolong(e, u.N) in one fused launch (multigrid.py:184)."""
+    if u.N != 2 * e.N or u.dim != e.dim:
+        raise ValueError(f"fine_N must be 2*{e.N}, got {u.N}")
+    lib = _lib.load()
+    code = _dtype_code(u.values)
+    stream = _stream_for(u.values)
+    x = _Arr(u.values, code)
+    ee = _Arr(_same_side(u.values, e.values), code)
+    out = _empty_like(u.values, tuple(u.values.shape))
+    o = _Arr(out, code)
+    _lib.check(lib.spaimg_prolong_correct(code, u.dim, u.N, x.ptr, ee.ptr, o.ptr, stream))
+    return Grid(u.N, out)
+
+
+def residual_norm(u: Grid, b: Grid) -> float:
+    """||b - A u||_2 (multigrid.py:207 / :214)."""
+    if u.N != b.N or u.dim != b.dim:
+        raise ValueError("u and b must live on the same grid")
+    lib = _lib.load()
+    code = _dtype_code(u.values)
+    stream = _stream_for(u.values)
+    x = _Arr(u.values, code)
+    bb = _Arr(_same_side(u.values, b.values), code)
+    out = ctypes.c_double(0.0)
+    _lib.check(lib.spaimg_residual_norm(code, u.dim, u.N, x.ptr, bb.ptr, ctypes.byref(out), stream))
+    return float(out.value)
+
+
+# ------------------------------------------------------------------------------------------
+# cycles
+# ------------------------------------------------------------------------------------------
+_LU_CACHE = {}
+
+
+def _coarsest_lu(dim: int, N: int):
+    """lu_factor of the assembled coarse Laplacian, cached (multigrid.py:147-149).
+    Host-side setup: the substitution itself runs on the GPU (K5)."""
+    key = (dim, N)
+    if key not in _LU_CACHE:
+        from scipy.linalg import lu_factor
+        lu, piv = lu_factor(laplacian(dim).to_matrix(N).toarray())
+        _LU_CACHE[key] = (np.ascontiguousarray(lu, dtype=np.float64),
+                          np.ascontiguousarray(piv, dtype=np.int32))
+    return _LU_CACHE[key]
+
+
+def _coarse_level(N: int, coarsest_N: int) -> int:
+    """Mesh count at which the recursion solves directly (multigrid.py:166, :178), raising the
+    reference's restrict() errors if a halving is impossible on the way (:112-115)."""
+    while N > coarsest_N:
+        if N % 2:
+            raise ValueError(f"cannot halve an odd mesh count N={N}")
+        if N // 2 < 2:
+            raise ValueError("coarse mesh would have no interior points")
+        N //= 2
+    return N
+
+
+def _mg_struct(cfg: MgConfig, dim: int, N: int, dtype_code: int):
+    M, omega = cfg.resolve_smoother()
+    if M.dim != dim:
+        raise ValueError(f"smoother dim {M.dim} != grid dim {dim}")
+    Nc = _coarse_level(N, cfg.coarsest_N)
+    lu, piv = _coarsest_lu(dim, Nc)
+    c = _lib.SpaimgMgConfig()
+    c.dtype = dtype_code
+    c.dim = dim
+    c.N = N
+    c.M = _stencil_struct(M)
+    c.omega = omega
+    c.gamma = 2 if cfg.cycle == "W" else 1
+    c.nu1 = int(cfg.nu1)
+    c.nu2 = int(cfg.nu2)
+    c.coarsest_N = int(cfg.coarsest_N)
+    c.coarse_N = Nc
+    c.coarse_n = int(lu.shape[0])
+    c.coarse_lu = lu.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    c.coarse_piv = piv.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
+    return c, (lu, piv)
+
+
+def cycle(u: Grid, b: Grid, cfg: MgConfig) -> Grid:
+    """One multigrid cycle for A*u = b at the grid's resolution (multigrid.py:157-185)."""
+    if u.N != b.N or u.dim != b.dim:
+        raise ValueError("u and b must live on the same grid")
+    lib = _lib.load()
+    code = _dtype_code(u.values)
+    if u.N > cfg.coarsest_N:
+        cfg.resolve_smoother()  # reference raises here before anything else (multigrid.py:169)
+    c, keep = _mg_struct(cfg, u.dim, u.N, code)
+    stream = _stream_for(u.values)
+    x = _Arr(u.values, code)
+    bb = _Arr(_same_side(u.values, b.values), code)
+    out = _empty_like(u.values, tuple(u.values.shape))
+    o = _Arr(out, code)
+    _lib.check(lib.spaimg_cycle(ctypes.byref(c), x.ptr, bb.ptr, o.ptr, stream))
+    return Grid(u.N, out)
+
+
+def _check_solve(b: Grid, cfg: MgConfig):
+    levels = b.N // cfg.coarsest_N
+    if levels * cfg.coarsest_N != b.N or levels & (levels - 1):
+        raise ValueError(f"N={b.N} must equal coarsest_N={cfg.coarsest_N} times a power of 2")
+    M, _ = cfg.resolve_smoother()
+    if M.dim != b.dim:
+        raise ValueError(f"smoother dim {M.dim} != problem dim {b.dim}")
+
+
+def _start_values(b: Grid, cfg: MgConfig, u0):
+    """The start iterate: the reference's seeded U(0,1) draw (multigrid.py:204-205) when
+    u0 is None; None (zero start, no upload) when u0 is 0; else the given values."""
+    if u0 is None:
+        rng = np.random.default_rng(cfg.rng_seed)
+        return _same_side(b.values, rng.uniform(0.0, 1.0, size=tuple(b.values.shape)))
+    if isinstance(u0, (int, float)) and u0 == 0:
+        return None
+    vals = u0.values if hasattr(u0, "values") else u0
+    if tuple(vals.shape) != tuple(b.values.shape):
+        raise ValueError("u0 must have the shape of b")
+    return _same_side(b.values, vals)
+
+
+def solve(b: Grid, cfg: MgConfig, u0=None) -> tuple:
+    """Run cycles from the start until ||r_k|| <= tol ||r_0|| or max_iters (multigrid.py:188-227).
+
+    Returns (solution Grid, SolveReport); rho_hat = (||r_K|| / ||r_0||)**(1/K).
+    """
+    _check_solve(b, cfg)
+    lib = _lib.load()
+    code = _dtype_code(b.values)
+    c, keep = _mg_struct(cfg, b.dim, b.N, code)
+    stream = _stream_for(b.values)
+    t0 = time.perf_counter()
+    start = _start_values(b, cfg, u0)
+    bb = _Arr(b.values, code)
+    uu = _Arr(start, code) if start is not None else None
+    out = _empty_like(b.values, tuple(b.values.shape))
+    o = _Arr(out, code)
+    norms = (ctypes.c_double * (cfg.max_iters + 1))()
+    iters = ctypes.c_int(0)
+    conv = ctypes.c_int(0)
+    _lib.check(lib.spaimg_solve(ctypes.byref(c), bb.ptr, uu.ptr if uu else None, o.ptr, float(cfg.tol),
+                                int(cfg.max_iters), norms, ctypes.byref(iters), ctypes.byref(conv), stream))
+    k = iters.value
+    hist = [float(norms[i]) for i in range(k + 1)]
+    rho_hat = (hist[-1] / hist[0]) ** (1.0 / k) if k else float("nan")
+    report = SolveReport(iterations=k, residual_norms=hist, rho_hat=float(rho_hat), converged=bool(conv.value),
+                         wall_time=time.perf_counter() - t0)
+    return Grid(b.N, out), report
+
+
+# ------------------------------------------------------------------------------------------
+# persistent solver handle (bench / repeated solves)
+# ------------------------------------------------------------------------------------------
+class Solver:
+    """Owns the device level hierarchy and the captured cycle graph for one (cfg, N, dtype)."""
+
+    def __init__(self, cfg: MgConfig, dim: int, N: int, dtype: str = "float64", device=0):
+        self.cfg = cfg
+        self.dim = dim
+        self.N = N
+        self.dtype_code = _lib.F32 if dtype in ("float32", "f32", "fp32") else _lib.F64
+        self.lib = _lib.load()
+        _lib.check(self.lib.spaimg_set_device(int(device)))
+        c, self._keep = _mg_struct(cfg, dim, N, self.dtype_code)
+        self._cfg_struct = c
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.spaimg_solver_create(ctypes.byref(c), ctypes.byref(h)))
+        self.handle = h
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            self.lib.spaimg_solver_destroy(h)
+            self.handle = None
+
+    @staticmethod
+    def _stream(stream):
+        if stream is None:
+            import torch
+            return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        return ctypes.c_void_p(stream)
+
+    def _ptr(self, values):
+        if values is None:
+            return None, None
+        a = _Arr(values, self.dtype_code)
+        return a, a.ptr
+
+    def load(self, b_values, u0_values=None, stream=None):
+        bk, bp = self._ptr(b_values)
+        uk, up = self._ptr(u0_values)
+        _lib.check(self.lib.spaimg_solver_load(self.handle, bp, up, self._stream(stream)))
+
+    def cycles(self, n, stream=None):
+        _lib.check(self.lib.spaimg_solver_cycles(self.handle, int(n), self._stream(stream)))
+
+    def run(self, tol=None, max_iters=None, stream=None):
+        tol = self.cfg.tol if tol is None else tol
+        max_iters = self.cfg.max_iters if max_iters is None else max_iters
+        norms = (ctypes.c_double * (max_iters + 1))()
+        iters = ctypes.c_int(0)
+        conv = ctypes.c_int(0)
+        _lib.check(self.lib.spaimg_solver_run(self.handle, float(tol), int(max_iters), norms, ctypes.byref(iters),
+                                              ctypes.byref(conv), self._stream(stream)))
+        k = iters.value
+        return [float(norms[i]) for i in range(k + 1)], k, bool(conv.value)
+
+    def store(self, out_values, stream=None):
+        ok, op = self._ptr(out_values)
+        _lib.check(self.lib.spaimg_solver_store(self.handle, op, self._stream(stream)))
+
+    def op(self, which, reps=1, stream=None):
+        _lib.check(self.lib.spaimg_solver_op(self.handle, int(which), int(reps), self._stream(stream)))
+
+    def stats(self) -> dict:
+        st = _lib.SpaimgSolverStats()
+        _lib.check(self.lib.spaimg_solver_stats_get(self.handle, ctypes.byref(st)))
+        return {f: getattr(st, f) for f, _ in st._fields_}
