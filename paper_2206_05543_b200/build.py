@@ -18,7 +18,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libspaimg_cuda.so")
 
 SOURCES = ["kernels_basic.cu", "kernels_sweep.cu", "solver.cu"]
-HEADERS = ["spaimg_common.cuh", "kernels.h"]
+HEADERS = ["spaimg_common.cuh", "kernels.h", "ptx.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [

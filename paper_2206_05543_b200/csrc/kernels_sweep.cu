@@ -4,6 +4,9 @@
 // halo in shared memory, then x' = x + omega * ((M r) * sM) from that tile in the same pass.
 // r is forced to zero outside the interior (the reference zero-pads r itself, stencils.py:146).
 #include "kernels.h"
+#include "ptx.cuh"
+
+#include <cstdlib>
 
 namespace spaimg {
 
@@ -114,6 +117,276 @@ __global__ void __launch_bounds__(256) k_sweep3d_tile(Layout L, const T* __restr
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// K1 2D: row-marching sweep.  A CTA owns a strip of W columns and a chunk of rows; one producer
+// warp streams (x row, b row) pairs of the strip plus a VEC-wide halo into a ring of shared-
+// memory stages with 1-D bulk copies (cp.async.bulk -> UBLKCP) completing on mbarriers.  Each
+// consumer lane owns VEC = 16/sizeof(T) adjacent columns and keeps x(j-1..j+1) and r(j-2..j)
+// of them in registers while marching down the rows; horizontal neighbours come from warp
+// shuffles, warp-edge neighbours from a tiny shared edge ring, the two strip-halo residuals
+// from the producer warp.  r is computed once per point; HBM traffic is x + b + x' (24 B/pt
+// fp64) plus the (W+2VEC)/W column halo and the 4-row chunk priming, both L2 hits.
+// ------------------------------------------------------------------------------------------
+template <class T> struct V16;
+template <> struct V16<double> {
+    using type = double2;
+    static __device__ __forceinline__ void ld(const double* p, double* v) {
+        const double2 t = *reinterpret_cast<const double2*>(p);
+        v[0] = t.x;
+        v[1] = t.y;
+    }
+    static __device__ __forceinline__ void st(double* p, const double* v) {
+        *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+    }
+};
+template <> struct V16<float> {
+    using type = float4;
+    static __device__ __forceinline__ void ld(const float* p, float* v) {
+        const float4 t = *reinterpret_cast<const float4*>(p);
+        v[0] = t.x;
+        v[1] = t.y;
+        v[2] = t.z;
+        v[3] = t.w;
+    }
+    static __device__ __forceinline__ void st(float* p, const float* v) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+};
+
+constexpr int M2_NW = 4;   // consumer warps per CTA
+constexpr int M2_ST = 6;   // (x row, b row) ring depth; the step loop is unrolled by M2_ST
+
+template <class T>
+__host__ __device__ constexpr int m2_vec() { return 16 / (int)sizeof(T); }
+template <class T>
+__host__ __device__ constexpr int m2_width() { return 32 * m2_vec<T>() * M2_NW; }
+template <class T>
+__host__ __device__ constexpr int m2_rowlen() { return m2_width<T>() + 2 * m2_vec<T>(); }
+template <class T>
+constexpr size_t m2_smem_bytes() {
+    return (size_t)2 * M2_ST * m2_rowlen<T>() * sizeof(T)   // x and b stages
+           + (size_t)2 * m2_rowlen<T>() * sizeof(T)         // r rows (ring of 2)
+           + (size_t)M2_ST * 8;                             // mbarriers
+}
+
+// value of r row (o0 = -1, 0, +1 -> rm, rc, rp) at column v + o1 of this lane
+template <class T, int VEC>
+__device__ __forceinline__ T pick(const T* rm, const T* rc, const T* rp, T lm, T lc, T lp, T hm, T hc, T hp, int o0,
+                                  int o1, int v) {
+    const T* row = o0 < 0 ? rm : (o0 == 0 ? rc : rp);
+    if (o1 == 0) return row[v];
+    if (o1 < 0) return v > 0 ? row[v - 1] : (o0 < 0 ? lm : (o0 == 0 ? lc : lp));
+    return v + 1 < VEC ? row[v + 1] : (o0 < 0 ? hm : (o0 == 0 ? hc : hp));
+}
+
+template <class T>
+struct M2Ctx {
+    T* xs;
+    T* bs;
+    T* rr;
+    uint64_t* full;
+    const T* xrow0;
+    const T* brow0;
+    T* orow0;  // output row 0, own first column
+    long long px;
+    int n, c0, col, sidx, q0, q_last, r0, lane;
+    bool producer, last_strip;
+};
+
+template <class T, int S, bool FZ>
+__device__ __forceinline__ void m2_issue(const M2Ctx<T>& c, int q, int slot) {
+    constexpr int RW = m2_rowlen<T>();
+    constexpr uint32_t row_bytes = RW * sizeof(T);
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&c.full[slot], FZ ? row_bytes : 2 * row_bytes);
+    if (!FZ) bulk_g2s(c.xs + slot * RW, c.xrow0 + (long long)q * c.px, row_bytes, &c.full[slot]);
+    bulk_g2s(c.bs + slot * RW, c.brow0 + (long long)q * c.px, row_bytes, &c.full[slot]);
+}
+
+// One marching step k (row j = q0 + k): r(j) for the strip (+ halo), then output row j-1.
+// P = k mod 6 makes every stage slot and register-row index a compile-time constant.
+template <class T, int S, bool FZ, int P>
+__device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_vec<T>()], T (&R)[3][m2_vec<T>()],
+                                        T (&RL)[3], T (&RH)[3], const Terms<T>& M, T sA, T sM, T omega) {
+    using O = Op<T>;
+    constexpr int VEC = m2_vec<T>();
+    constexpr int W = m2_width<T>();
+    constexpr int RW = m2_rowlen<T>();
+    constexpr int ST = M2_ST;
+    constexpr int sj = P % ST, sp = (P + 1) % ST, sm = (P + ST - 1) % ST;  // stage slots of rows j, j+1, j-1
+    constexpr int ic = P % 3, ip = (P + 1) % 3, im = (P + 2) % 3;          // register rows j, j+1, j-1
+    constexpr int rs = P % 2;                                               // r row ring slot
+    const int j = c.q0 + k;
+    mbar_wait(&c.full[sp], (uint32_t)(((k + 1) / ST) & 1));
+    const bool row_in = (unsigned)j < (unsigned)c.n;
+    T* rrow = c.rr + rs * RW;
+    if (!c.producer) {
+        T bj[VEC];
+        V16<T>::ld(c.bs + sj * RW + c.sidx, bj);
+        if constexpr (FZ) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) R[ic][v] = bj[v];  // b - A 0 == b exactly
+        } else {
+            V16<T>::ld(c.xs + sp * RW + c.sidx, X[ip]);
+            const T left = c.xs[sj * RW + c.sidx - 1];
+            const T right = c.xs[sj * RW + c.sidx + VEC];
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+                const T xe = v + 1 < VEC ? X[ic][v + 1] : right;
+                const T xw = v > 0 ? X[ic][v - 1] : left;
+                R[ic][v] = residual2d<T>(bj[v], X[ic][v], X[ip][v], X[im][v], xe, xw, sA);
+            }
+        }
+        if (!row_in || c.last_strip) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v)
+                if (!row_in || c.col + v >= c.n) R[ic][v] = T(0);  // r is zero outside the interior
+        }
+        V16<T>::st(rrow + c.sidx, R[ic]);
+    } else if (c.lane < 2) {
+        // strip-halo residuals at columns c0-1 (lane 0) and c0+W (lane 1)
+        const int si = c.lane == 0 ? VEC - 1 : VEC + W;
+        const int cc = c.lane == 0 ? c.c0 - 1 : c.c0 + W;
+        T rv;
+        if constexpr (FZ) {
+            rv = c.bs[sj * RW + si];
+        } else {
+            rv = residual2d<T>(c.bs[sj * RW + si], c.xs[sj * RW + si], c.xs[sp * RW + si], c.xs[sm * RW + si],
+                               c.xs[sj * RW + si + 1], c.xs[sj * RW + si - 1], sA);
+        }
+        if (!row_in || cc < 0 || cc >= c.n) rv = T(0);
+        rrow[si] = rv;
+    }
+    named_bar_sync(1, (M2_NW + 1) * 32);
+    if (c.producer) {
+        // stage j-1 was last read before this barrier: refill its slot with row j-1+ST
+        if (c.lane == 0 && j - 1 + ST <= c.q_last) m2_issue<T, S, FZ>(c, j - 1 + ST, sm);
+        return;
+    }
+    RL[ic] = rrow[c.sidx - 1];
+    RH[ic] = rrow[c.sidx + VEC];
+    if (j - 1 < c.r0) return;
+    // output row j-1: r rows j-2 (R[ip]), j-1 (R[im]), j (R[ic])
+    T out[VEC];
+    const int nt = tnt<T, S>(M);
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+        T acc = T(0);
+#pragma unroll
+        for (int t = 0; t < (S == SHAPE_GENERIC ? kMaxTerms : ShapeT<(S == SHAPE_GENERIC ? 1 : S)>::nt); ++t) {
+            if (S == SHAPE_GENERIC && t >= nt) break;
+            const T val = pick<T, VEC>(R[ip], R[im], R[ic], RL[ip], RL[im], RL[ic], RH[ip], RH[im], RH[ic],
+                                       toff<T, S>(M, t, 0), toff<T, S>(M, t, 1), v);
+            acc = O::add(acc, O::mul(M.c[t], val));
+        }
+        out[v] = relax<T>(FZ ? T(0) : X[im][v], acc, sM, omega);
+    }
+    T* dst = c.orow0 + (long long)(j - 1) * c.px;
+    if (!c.last_strip || c.col + VEC <= c.n) {
+        V16<T>::st(dst, out);
+    } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v)
+            if (c.col + v < c.n) dst[v] = out[v];
+    }
+}
+
+template <class T, int S, bool FZ>
+__global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, const T* __restrict__ x,
+                                                                     const T* __restrict__ b, T* __restrict__ xo,
+                                                                     Terms<T> M, T sA, T sM, T omega, int rows) {
+    constexpr int VEC = m2_vec<T>();
+    constexpr int W = m2_width<T>();
+    constexpr int RW = m2_rowlen<T>();
+    constexpr int ST = M2_ST;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    M2Ctx<T> c;
+    c.xs = reinterpret_cast<T*>(smem_raw);
+    c.bs = c.xs + ST * RW;
+    c.rr = c.bs + ST * RW;
+    c.full = reinterpret_cast<uint64_t*>(c.rr + 2 * RW);
+    const int warp = threadIdx.x >> 5;
+    c.lane = threadIdx.x & 31;
+    c.producer = warp == M2_NW;
+    c.n = L.n;
+    c.px = L.px;
+    c.c0 = blockIdx.x * W;
+    c.r0 = blockIdx.y * rows;
+    const int r_end = min(c.r0 + rows, c.n);
+    c.q0 = c.r0 - 2;        // first staged row
+    c.q_last = r_end + 1;   // last staged row
+    c.last_strip = c.c0 + W > c.n;
+    c.sidx = VEC + (c.producer ? 0 : warp) * 32 * VEC + c.lane * VEC;
+    c.col = c.c0 + (c.producer ? 0 : warp) * 32 * VEC + c.lane * VEC;
+    c.xrow0 = x + L.origin + (c.c0 - VEC);
+    c.brow0 = b + L.origin + (c.c0 - VEC);
+    c.orow0 = xo + L.origin + c.col;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < ST; ++i) mbar_init(&c.full[i], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (c.producer && c.lane == 0)
+        for (int q = c.q0; q < c.q0 + ST && q <= c.q_last; ++q) m2_issue<T, S, FZ>(c, q, q - c.q0);
+
+    T X[3][VEC], R[3][VEC], RL[3], RH[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        RL[i] = RH[i] = T(0);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) X[i][v] = R[i][v] = T(0);
+    }
+    mbar_wait(&c.full[0], 0);
+    mbar_wait(&c.full[1], 0);
+    if (!FZ && !c.producer) {
+        V16<T>::ld(c.xs + 0 * RW + c.sidx, X[0]);  // x(q0)   = x(j-1) of step k = 1
+        V16<T>::ld(c.xs + 1 * RW + c.sidx, X[1]);  // x(q0+1) = x(j)
+    }
+    const int K = r_end - c.q0;  // steps k = 1 .. K  (rows j = r0-1 .. r_end)
+    for (int kb = 0; kb <= K; kb += ST) {
+        if (kb >= 1) m2_step<T, S, FZ, 0>(c, kb, X, R, RL, RH, M, sA, sM, omega);
+        if (kb + 1 <= K) m2_step<T, S, FZ, 1>(c, kb + 1, X, R, RL, RH, M, sA, sM, omega);
+        if (kb + 2 <= K) m2_step<T, S, FZ, 2>(c, kb + 2, X, R, RL, RH, M, sA, sM, omega);
+        if (kb + 3 <= K) m2_step<T, S, FZ, 3>(c, kb + 3, X, R, RL, RH, M, sA, sM, omega);
+        if (kb + 4 <= K) m2_step<T, S, FZ, 4>(c, kb + 4, X, R, RL, RH, M, sA, sM, omega);
+        if (kb + 5 <= K) m2_step<T, S, FZ, 5>(c, kb + 5, X, R, RL, RH, M, sA, sM, omega);
+    }
+}
+
+static int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+template <class T, int S, bool FZ>
+static cudaError_t launch_sweep2d_march(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA,
+                                        T sM, T omega, cudaStream_t s) {
+    constexpr size_t smem = m2_smem_bytes<T>();
+    constexpr int threads = (M2_NW + 1) * 32;
+    static int occ = 0;
+    if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep2d_march<T, S, FZ>, threads, smem);
+        if (occ <= 0) occ = 1;
+    }
+    const int W = m2_width<T>();
+    const int strips = (L.n + W - 1) / W;
+    const int slots = num_sms() * occ;
+    int chunks = (slots + strips - 1) / strips;
+    int rows = (L.n + chunks - 1) / chunks;
+    if (rows < 16) rows = 16;
+    chunks = (L.n + rows - 1) / rows;
+    dim3 g(strips, chunks);
+    k_sweep2d_march<T, S, FZ><<<g, threads, smem, s>>>(L, x, b, xo, M, sA, sM, omega, rows);
+    return cudaGetLastError();
+}
+
 bool sweep_fused_supported(int dim, int shape) {
     if (dim == 2) return shape == SHAPE_GENERIC || shape == SHAPE_C1 || shape == SHAPE_STAR5 || shape == SHAPE_BOX9;
     return shape == SHAPE_GENERIC || shape == SHAPE_C1 || shape == SHAPE_STAR7;
@@ -123,8 +396,12 @@ template <class T, int S, bool FZ>
 static cudaError_t sweep_dispatch(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
                                   T omega, cudaStream_t s) {
     if (L.dim == 2) {
-        dim3 g((L.n + S2_TW - 1) / S2_TW, (L.n + S2_TH - 1) / S2_TH);
-        k_sweep2d_tile<T, S, FZ><<<g, 256, 0, s>>>(L, x, b, xo, M, sA, sM, omega);
+        if (getenv("SPAIMG_SWEEP_V1")) {
+            dim3 g((L.n + S2_TW - 1) / S2_TW, (L.n + S2_TH - 1) / S2_TH);
+            k_sweep2d_tile<T, S, FZ><<<g, 256, 0, s>>>(L, x, b, xo, M, sA, sM, omega);
+        } else {
+            return launch_sweep2d_march<T, S, FZ>(L, x, b, xo, M, sA, sM, omega, s);
+        }
     } else {
         dim3 g((L.n + S3_TX - 1) / S3_TX, (L.n + S3_TY - 1) / S3_TY, (L.n + S3_TZ - 1) / S3_TZ);
         k_sweep3d_tile<T, S, FZ><<<g, 256, 0, s>>>(L, x, b, xo, M, sA, sM, omega);

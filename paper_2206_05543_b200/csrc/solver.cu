@@ -143,12 +143,13 @@ struct Scratch {
 
 // copy a dense input (host or device) into a padded level buffer
 template <class T>
-static int load_dense(Scratch& sc, const Layout& L, const void* src, T* padded, cudaStream_t s) {
+static int load_dense(Scratch& sc, const Layout& L, const void* src, T* padded, cudaStream_t s,
+                      T* stage_buf = nullptr) {
     const long long cnt = count_of(L.dim, L.N);
     const T* dsrc = static_cast<const T*>(src);
     if (!is_device_ptr(src)) {
-        T* stage = nullptr;
-        CK(sc.get(&stage, (size_t)cnt));
+        T* stage = stage_buf;
+        if (!stage) CK(sc.get(&stage, (size_t)cnt));
         CK(cudaMemcpyAsync(stage, src, (size_t)cnt * sizeof(T), cudaMemcpyHostToDevice, s));
         dsrc = stage;
     }
@@ -158,14 +159,15 @@ static int load_dense(Scratch& sc, const Layout& L, const void* src, T* padded, 
 
 // copy a padded level buffer out to a dense destination (host or device)
 template <class T>
-static int store_dense(Scratch& sc, const Layout& L, const T* padded, void* dst, cudaStream_t s) {
+static int store_dense(Scratch& sc, const Layout& L, const T* padded, void* dst, cudaStream_t s,
+                       T* stage_buf = nullptr) {
     const long long cnt = count_of(L.dim, L.N);
     if (is_device_ptr(dst)) {
         CK(launch_unpad<T>(L, padded, static_cast<T*>(dst), s));
         return 0;
     }
-    T* stage = nullptr;
-    CK(sc.get(&stage, (size_t)cnt));
+    T* stage = stage_buf;
+    if (!stage) CK(sc.get(&stage, (size_t)cnt));
     CK(launch_unpad<T>(L, padded, stage, s));
     CK(cudaMemcpyAsync(dst, stage, (size_t)cnt * sizeof(T), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -583,10 +585,10 @@ template <class T> struct Solver final : spaimg_solver {
         Scratch sc(s);
         Level<T>& L = lv[0];
         if (b)  // NULL keeps the right-hand side already loaded
-            if (int rc = load_dense<T>(sc, L.L, b, L.b, s)) return rc;
+            if (int rc = load_dense<T>(sc, L.L, b, L.b, s, stage)) return rc;
         cur = 0;
         if (u0) {
-            if (int rc = load_dense<T>(sc, L.L, u0, L.x[0], s)) return rc;
+            if (int rc = load_dense<T>(sc, L.L, u0, L.x[0], s, stage)) return rc;
         } else {
             CK(cudaMemsetAsync(L.x[0], 0, (size_t)L.L.alloc * sizeof(T), s));
         }
@@ -626,7 +628,7 @@ template <class T> struct Solver final : spaimg_solver {
 
     int store(void* out, cudaStream_t s) override {
         Scratch sc(s);
-        return store_dense<T>(sc, lv[0].L, lv[0].x[cur], out, s);
+        return store_dense<T>(sc, lv[0].L, lv[0].x[cur], out, s, stage);
     }
 
     int op(int which, int reps, cudaStream_t s) override {
