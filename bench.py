@@ -273,8 +273,8 @@ def run_ours(args):
     # ---------------- roofline of the dominant kernel (fused sweep K1, finest level) --------
     reps = 20
     solver.load(None)
-    solver.op(0, 2)
-    t_k1 = time_events(lambda: solver.op(0, reps), stream, reps)
+    solver.op(0, reps)  # captures the cached replay graph
+    t_k1 = min(time_events(lambda: solver.op(0, reps), stream, reps) for _ in range(3))
     peak, peak_kind = peaks()
     esz = 8
     k1_bytes = 3 * esz * n0  # read x, read b, write x'
@@ -402,8 +402,8 @@ def run_extras(sp, torch, stream, peak):
         st = s3.stats()
         n0 = (N - 1) ** 3
         reps = 10
-        s3.op(0, 1)
-        tk = time_events(lambda: s3.op(0, reps), stream, reps)
+        s3.op(0, reps)
+        tk = min(time_events(lambda: s3.op(0, reps), stream, reps) for _ in range(3))
         out["c4_m7_V11"] = {"cycles": k, "converged": conv, "time_to_tol_ms": t * 1e3, "ms_per_cycle": t / k * 1e3,
                             "dof_per_s": n0 * k / t, "bytes_per_cycle": st["bytes_per_cycle"],
                             "vcycle_roofline_frac": st["bytes_per_cycle"] / (t / k) / 1e9 / peak,
@@ -438,7 +438,7 @@ def microbench(sp, torch, stream, peak):
             r = {}
             for op, name, bpu in ((0, "sweep", 3.0), (1, "residual_restrict", 2 + 2.0 ** -dim),
                                   (2, "prolong_correct", 2 + 2.0 ** -dim), (3, "residual_norm", 2.0)):
-                so.op(op, 2)
+                so.op(op, 5)
                 best = min(time_events(lambda: so.op(op, 5), stream, 5) for _ in range(3))
                 gbs = bpu * s * n / best / 1e9
                 r[name] = {"ms": best * 1e3, "gbs": gbs, "frac": gbs / peak, "bytes_per_unknown": bpu * s}

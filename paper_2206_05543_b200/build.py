@@ -17,8 +17,8 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libspaimg_cuda.so")
 
-SOURCES = ["kernels_basic.cu", "kernels_sweep.cu", "solver.cu"]
-HEADERS = ["spaimg_common.cuh", "kernels.h", "ptx.cuh"]
+SOURCES = ["kernels_basic.cu", "kernels_sweep.cu", "kernels_sweep3d.cu", "solver.cu"]
+HEADERS = ["spaimg_common.cuh", "kernels.h", "ptx.cuh", "march.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [

@@ -4,28 +4,12 @@
 // halo in shared memory, then x' = x + omega * ((M r) * sM) from that tile in the same pass.
 // r is forced to zero outside the interior (the reference zero-pads r itself, stencils.py:146).
 #include "kernels.h"
+#include "march.cuh"
 #include "ptx.cuh"
 
 #include <cstdlib>
 
 namespace spaimg {
-
-template <class T, int S>
-__device__ __forceinline__ int toff(const Terms<T>& M, int k, int a) {
-    if constexpr (S == SHAPE_GENERIC) {
-        return M.off[k][a];
-    } else {
-        return ShapeT<S>::o(k, a);
-    }
-}
-template <class T, int S>
-__device__ __forceinline__ int tnt(const Terms<T>& M) {
-    if constexpr (S == SHAPE_GENERIC) {
-        return M.nt;
-    } else {
-        return ShapeT<S>::nt;
-    }
-}
 
 __device__ __forceinline__ long long pidx2(const Layout& L, int i0, int i1) { return L.origin + (long long)i0 * L.px + i1; }
 __device__ __forceinline__ long long pidx3(const Layout& L, int i0, int i1, int i2) {
@@ -127,32 +111,6 @@ __global__ void __launch_bounds__(256) k_sweep3d_tile(Layout L, const T* __restr
 // from the producer warp.  r is computed once per point; HBM traffic is x + b + x' (24 B/pt
 // fp64) plus the (W+2VEC)/W column halo and the 4-row chunk priming, both L2 hits.
 // ------------------------------------------------------------------------------------------
-template <class T> struct V16;
-template <> struct V16<double> {
-    using type = double2;
-    static __device__ __forceinline__ void ld(const double* p, double* v) {
-        const double2 t = *reinterpret_cast<const double2*>(p);
-        v[0] = t.x;
-        v[1] = t.y;
-    }
-    static __device__ __forceinline__ void st(double* p, const double* v) {
-        *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
-    }
-};
-template <> struct V16<float> {
-    using type = float4;
-    static __device__ __forceinline__ void ld(const float* p, float* v) {
-        const float4 t = *reinterpret_cast<const float4*>(p);
-        v[0] = t.x;
-        v[1] = t.y;
-        v[2] = t.z;
-        v[3] = t.w;
-    }
-    static __device__ __forceinline__ void st(float* p, const float* v) {
-        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-    }
-};
-
 constexpr int M2_NW = 4;   // consumer warps per CTA
 constexpr int M2_ST = 6;   // (x row, b row) ring depth; the step loop is unrolled by M2_ST
 
@@ -354,17 +312,6 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, co
     }
 }
 
-static int num_sms() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
-
 template <class T, int S, bool FZ>
 static cudaError_t launch_sweep2d_march(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA,
                                         T sM, T omega, cudaStream_t s) {
@@ -393,6 +340,10 @@ bool sweep_fused_supported(int dim, int shape) {
 }
 
 template <class T, int S, bool FZ>
+cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
+                                 T omega, cudaStream_t s);
+
+template <class T, int S, bool FZ>
 static cudaError_t sweep_dispatch(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
                                   T omega, cudaStream_t s) {
     if (L.dim == 2) {
@@ -403,8 +354,13 @@ static cudaError_t sweep_dispatch(const Layout& L, const T* x, const T* b, T* xo
             return launch_sweep2d_march<T, S, FZ>(L, x, b, xo, M, sA, sM, omega, s);
         }
     } else {
-        dim3 g((L.n + S3_TX - 1) / S3_TX, (L.n + S3_TY - 1) / S3_TY, (L.n + S3_TZ - 1) / S3_TZ);
-        k_sweep3d_tile<T, S, FZ><<<g, 256, 0, s>>>(L, x, b, xo, M, sA, sM, omega);
+        if (getenv("SPAIMG_SWEEP_V1") || !(S == SHAPE_GENERIC || S == SHAPE_C1 || S == SHAPE_STAR7)) {
+            dim3 g((L.n + S3_TX - 1) / S3_TX, (L.n + S3_TY - 1) / S3_TY, (L.n + S3_TZ - 1) / S3_TZ);
+            k_sweep3d_tile<T, S, FZ><<<g, 256, 0, s>>>(L, x, b, xo, M, sA, sM, omega);
+        } else {
+            return launch_sweep3d_march<T, (S == SHAPE_GENERIC || S == SHAPE_C1 || S == SHAPE_STAR7) ? S : SHAPE_GENERIC,
+                                        FZ>(L, x, b, xo, M, sA, sM, omega, s);
+        }
     }
     return cudaGetLastError();
 }

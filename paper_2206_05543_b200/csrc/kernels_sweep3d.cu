@@ -1,0 +1,360 @@
+// K1 3D: plane-marching fused SPAI sweep (x' = x + omega M (b - A x), reference
+// multigrid.py:98-100) with TMA tensor-tile staging.
+//
+// A CTA owns a TY x TX tile of (axis1, axis2) and marches along axis 0 over a chunk of planes.
+// Thread 0 streams, per plane, the x tile with a 2-row / VEC-column halo and the b tile with a
+// 1-row halo into a 4-deep ring of shared-memory stages with cp.async.bulk.tensor.3d (SASS
+// UTMALDG) completing on mbarriers.  Each thread owns 2 rows x VEC columns and keeps
+// x(j-1..j+1) and r(j-2..j) of them in registers (register-blocked z-marching); r(j) of the
+// tile plus its one-point ring goes to a 3-plane shared ring from which M takes its in-plane
+// neighbours.  r is computed once per tile point (the ring is recomputed by the neighbour
+// tile: 2(TX+TY)/(TX*TY) extra).  The step loop is unrolled by 12 = lcm(4 stages, 3 rows) so
+// every ring index is a compile-time constant.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "kernels.h"
+#include "march.cuh"
+#include "ptx.cuh"
+
+namespace spaimg {
+
+constexpr int M3_TY = 16;  // tile rows (axis 1)
+constexpr int M3_NW = 8;   // warps; each owns 2 tile rows
+constexpr int M3_ST = 4;   // TMA stage ring depth
+constexpr int M3_RR = 3;   // r plane ring depth
+constexpr int M3_THREADS = M3_NW * 32;
+
+template <class T> struct M3 {
+    static constexpr int VEC = 16 / (int)sizeof(T);
+    static constexpr int TX = 32 * VEC;            // tile columns (axis 2)
+    static constexpr int TY = M3_TY;
+    static constexpr int RW = TX + 2 * VEC;        // staged row length
+    static constexpr int XR = TY + 4;              // x stage rows  [y0-2, y0+TY+2)
+    static constexpr int BR = TY + 2;              // b stage rows  [y0-1, y0+TY+1)
+    static constexpr int RR = TY + 2;              // r plane rows  [y0-1, y0+TY+1)
+    static constexpr int al(int e) { return (e * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T); }
+    static constexpr int XS = al(XR * RW);         // elements per x stage (128-B multiple)
+    static constexpr int BS = al(BR * RW);
+    static constexpr int RS = al(RR * RW);
+    static constexpr int NRING = 2 * TX + 2 * TY + 4;
+    static constexpr size_t smem = (size_t)(M3_ST * (XS + BS) + M3_RR * RS) * sizeof(T) + M3_ST * 8;
+};
+
+template <class T>
+struct M3Ctx {
+    T* xs;
+    T* bs;
+    T* rr;
+    uint64_t* full;
+    T* obase;  // output at (plane 0, own row 0, own column)
+    long long px, pp;
+    int n, x0, y0, q0, q_last, z0, yl, xl, tid;
+    bool edge;  // tile touches the right/bottom boundary (masking needed)
+    int cx, cy;  // TMA coordinates of the tile's stage origin (x stage)
+};
+
+template <class T, bool FZ>
+__device__ __forceinline__ void m3_issue(const M3Ctx<T>& c, const CUtensorMap* xm, const CUtensorMap* bm, int q,
+                                         int slot) {
+    using G = M3<T>;
+    constexpr uint32_t xb = G::XR * G::RW * sizeof(T), bb = G::BR * G::RW * sizeof(T);
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&c.full[slot], FZ ? bb : xb + bb);
+    if (!FZ) tma_load_3d(c.xs + slot * G::XS, xm, c.cx, c.cy, kGhost + q, &c.full[slot]);
+    tma_load_3d(c.bs + slot * G::BS, bm, c.cx, c.cy + 1, kGhost + q, &c.full[slot]);
+}
+
+// r at a tile-local ring point (ry, rx) of plane j, all operands from shared memory
+template <class T, bool FZ>
+__device__ __forceinline__ T m3_ring_r(const M3Ctx<T>& c, int sj, int sp, int sm, int ry, int rx, int j, T sA) {
+    using G = M3<T>;
+    const int gy = c.y0 + ry, gx = c.x0 + rx;
+    if ((unsigned)j >= (unsigned)c.n || (unsigned)gy >= (unsigned)c.n || (unsigned)gx >= (unsigned)c.n) return T(0);
+    const T b = c.bs[sj * G::BS + (ry + 1) * G::RW + G::VEC + rx];
+    if constexpr (FZ) {
+        return b;
+    } else {
+        const T* xj = c.xs + sj * G::XS + (ry + 2) * G::RW + G::VEC + rx;
+        const T xp0 = c.xs[sp * G::XS + (ry + 2) * G::RW + G::VEC + rx];
+        const T xm0 = c.xs[sm * G::XS + (ry + 2) * G::RW + G::VEC + rx];
+        return residual3d<T>(b, xj[0], xp0, xm0, xj[G::RW], xj[-G::RW], xj[1], xj[-1], sA);
+    }
+}
+
+template <class T, int S, bool FZ, int P>
+__device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xmap, const CUtensorMap* bmap, int k,
+                                        T (&X)[3][2][M3<T>::VEC], T (&R)[3][2][M3<T>::VEC], const Terms<T>& M,
+                                        T sA, T sM, T omega) {
+    using G = M3<T>;
+    using O = Op<T>;
+    constexpr int VEC = G::VEC;
+    constexpr int RW = G::RW;
+    constexpr int sj = P % M3_ST, sp = (P + 1) % M3_ST, sm = (P + M3_ST - 1) % M3_ST;
+    constexpr int ic = P % 3, ip = (P + 1) % 3, im = (P + 2) % 3;
+    constexpr int rj = P % M3_RR, rj1 = (P + 2) % M3_RR, rj2 = (P + 1) % M3_RR;  // r ring: planes j, j-1, j-2
+    const int j = c.q0 + k;
+    // generic shapes read r(j-3)'s ring slot in the previous step's output phase
+    if constexpr (S == SHAPE_GENERIC) __syncthreads();
+    mbar_wait(&c.full[sp], (uint32_t)(((k + 1) / M3_ST) & 1));
+    const bool plane_in = (unsigned)j < (unsigned)c.n;
+
+    // ---- r(j) at the two owned rows -------------------------------------------------------
+    T* rpl = c.rr + rj * G::RS;
+#pragma unroll
+    for (int yy = 0; yy < 2; ++yy) {
+        const int row = c.yl + yy;
+        T bj[VEC];
+        V16<T>::ld(c.bs + sj * G::BS + (row + 1) * RW + VEC + c.xl, bj);
+        if constexpr (FZ) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) R[ic][yy][v] = bj[v];
+        } else {
+            const T* xrow = c.xs + sj * G::XS + (row + 2) * RW + VEC + c.xl;
+            V16<T>::ld(c.xs + sp * G::XS + (row + 2) * RW + VEC + c.xl, X[ip][yy]);
+            T up[VEC], dn[VEC];
+            if (yy == 0) {
+                V16<T>::ld(xrow - RW, up);
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) dn[v] = X[ic][1][v];
+            } else {
+                V16<T>::ld(xrow + RW, dn);
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) up[v] = X[ic][0][v];
+            }
+            const T left = xrow[-1], right = xrow[VEC];
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+                const T xe = v + 1 < VEC ? X[ic][yy][v + 1] : right;
+                const T xw = v > 0 ? X[ic][yy][v - 1] : left;
+                R[ic][yy][v] = residual3d<T>(bj[v], X[ic][yy][v], X[ip][yy][v], X[im][yy][v], dn[v], up[v], xe, xw, sA);
+            }
+        }
+        if (!plane_in || c.edge) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v)
+                if (!plane_in || c.y0 + row >= c.n || c.x0 + c.xl + v >= c.n) R[ic][yy][v] = T(0);
+        }
+        V16<T>::st(rpl + (row + 1) * RW + VEC + c.xl, R[ic][yy]);
+    }
+    // ---- r(j) on the one-point ring of the tile, spread over all warps ------------------------
+    {
+        const int lane = c.tid & 31, w = c.tid >> 5;
+#pragma unroll
+        for (int base = 0; base < G::NRING; base += M3_THREADS) {
+            const int i = base + lane * M3_NW + w;
+            if (i < G::NRING) {
+                int ry, rx;
+                if (i < G::TX) {
+                    ry = -1, rx = i;
+                } else if (i < 2 * G::TX) {
+                    ry = G::TY, rx = i - G::TX;
+                } else if (i < 2 * G::TX + G::TY) {
+                    ry = i - 2 * G::TX, rx = -1;
+                } else if (i < 2 * G::TX + 2 * G::TY) {
+                    ry = i - 2 * G::TX - G::TY, rx = G::TX;
+                } else {
+                    const int q = i - 2 * G::TX - 2 * G::TY;
+                    ry = (q & 2) ? G::TY : -1;
+                    rx = (q & 1) ? G::TX : -1;
+                }
+                rpl[(ry + 1) * RW + VEC + rx] = m3_ring_r<T, FZ>(c, sj, sp, sm, ry, rx, j, sA);
+            }
+        }
+    }
+    __syncthreads();
+    if (c.tid == 0 && j - 1 + M3_ST <= c.q_last) m3_issue<T, FZ>(c, xmap, bmap, j - 1 + M3_ST, sm);
+    if (j - 1 < c.z0) return;
+
+    // ---- output plane j-1 -------------------------------------------------------------------
+    const T* r1 = c.rr + rj1 * G::RS;  // r(j-1)
+    const T* r0 = c.rr + rj * G::RS;   // r(j)
+    const T* r2 = c.rr + rj2 * G::RS;  // r(j-2)
+    const int nt = tnt<T, S>(M);
+#pragma unroll
+    for (int yy = 0; yy < 2; ++yy) {
+        const int row = c.yl + yy;
+        const int so = (row + 1) * RW + VEC + c.xl;  // own position in an r plane
+        T out[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+            T acc = T(0);
+#pragma unroll
+            for (int t = 0; t < (S == SHAPE_GENERIC ? kMaxTerms : ShapeT<(S == SHAPE_GENERIC ? 1 : S)>::nt); ++t) {
+                if (S == SHAPE_GENERIC && t >= nt) break;
+                const int o0 = toff<T, S>(M, t, 0), o1 = toff<T, S>(M, t, 1), o2 = toff<T, S>(M, t, 2);
+                T val;
+                if (o1 == 0 && o2 == 0) {
+                    val = o0 == 0 ? R[im][yy][v] : (o0 > 0 ? R[ic][yy][v] : R[ip][yy][v]);
+                } else if (o0 == 0 && o2 == 0 && ((o1 > 0 && yy == 0) || (o1 < 0 && yy == 1))) {
+                    val = R[im][1 - yy][v];  // in-plane row neighbour held by this thread
+                } else if (o0 == 0 && o1 == 0 && v + o2 >= 0 && v + o2 < VEC) {
+                    val = R[im][yy][v + o2];
+                } else {
+                    const T* pl = o0 == 0 ? r1 : (o0 > 0 ? r0 : r2);
+                    val = pl[so + o1 * RW + v + o2];
+                }
+                acc = O::add(acc, O::mul(M.c[t], val));
+            }
+            out[v] = relax<T>(FZ ? T(0) : X[im][yy][v], acc, sM, omega);
+        }
+        T* dst = c.obase + (long long)(j - 1) * c.pp + (long long)yy * c.px;
+        if (!c.edge) {
+            V16<T>::st(dst, out);
+        } else if (c.y0 + row < c.n) {
+            if (c.x0 + c.xl + VEC <= c.n) {
+                V16<T>::st(dst, out);
+            } else {
+#pragma unroll
+                for (int v = 0; v < VEC; ++v)
+                    if (c.x0 + c.xl + v < c.n) dst[v] = out[v];
+            }
+        }
+    }
+}
+
+template <class T, int S, bool FZ>
+__global__ void __launch_bounds__(M3_THREADS, 2)
+    k_sweep3d_march(Layout L, const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap bmap,
+                    const T* __restrict__ x, T* __restrict__ xo, Terms<T> M, T sA, T sM, T omega, int planes) {
+    using G = M3<T>;
+    constexpr int VEC = G::VEC;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    M3Ctx<T> c;
+    c.xs = reinterpret_cast<T*>(smem_raw);
+    c.bs = c.xs + M3_ST * G::XS;
+    c.rr = c.bs + M3_ST * G::BS;
+    c.full = reinterpret_cast<uint64_t*>(c.rr + M3_RR * G::RS);
+    c.tid = threadIdx.x;
+    c.n = L.n;
+    c.px = L.px;
+    c.pp = L.pp;
+    c.x0 = blockIdx.x * G::TX;
+    c.y0 = blockIdx.y * G::TY;
+    c.z0 = blockIdx.z * planes;
+    const int z_end = min(c.z0 + planes, c.n);
+    c.q0 = c.z0 - 2;
+    c.q_last = z_end + 1;
+    c.yl = (threadIdx.x >> 5) * 2;
+    c.xl = (threadIdx.x & 31) * VEC;
+    c.edge = c.x0 + G::TX > c.n || c.y0 + G::TY > c.n;
+    c.cx = (int)(L.origin % L.px) + c.x0 - VEC;  // LX + x0 - VEC
+    c.cy = kGhost + c.y0 - 2;
+    c.obase = xo + L.origin + (long long)(c.y0 + c.yl) * L.px + c.x0 + c.xl;
+
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&xmap);
+        tma_prefetch_desc(&bmap);
+        for (int i = 0; i < M3_ST; ++i) mbar_init(&c.full[i], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int q = c.q0; q < c.q0 + M3_ST && q <= c.q_last; ++q) m3_issue<T, FZ>(c, &xmap, &bmap, q, q - c.q0);
+
+    T X[3][2][VEC], R[3][2][VEC];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int yy = 0; yy < 2; ++yy)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) X[a][yy][v] = R[a][yy][v] = T(0);
+    mbar_wait(&c.full[0], 0);
+    mbar_wait(&c.full[1], 0);
+    if (!FZ) {
+#pragma unroll
+        for (int yy = 0; yy < 2; ++yy) {
+            V16<T>::ld(c.xs + 0 * G::XS + (c.yl + yy + 2) * G::RW + VEC + c.xl, X[0][yy]);
+            V16<T>::ld(c.xs + 1 * G::XS + (c.yl + yy + 2) * G::RW + VEC + c.xl, X[1][yy]);
+        }
+    }
+    const int K = z_end - c.q0;  // steps k = 1..K (planes j = z0-1 .. z_end)
+    for (int kb = 0; kb <= K; kb += 12) {
+#define M3STEP(p)                                                                            \
+    if (kb + (p) >= 1 && kb + (p) <= K)                                                     \
+        m3_step<T, S, FZ, (p)>(c, &xmap, &bmap, kb + (p), X, R, M, sA, sM, omega);
+        M3STEP(0) M3STEP(1) M3STEP(2) M3STEP(3) M3STEP(4) M3STEP(5)
+        M3STEP(6) M3STEP(7) M3STEP(8) M3STEP(9) M3STEP(10) M3STEP(11)
+#undef M3STEP
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// host side: tensor maps + launch
+// ------------------------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 3-D map over a whole padded level allocation (cols, rows, planes), box = (RW, rows, 1)
+template <class T>
+static cudaError_t make_map(CUtensorMap* map, const Layout& L, const T* base, int box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return cudaErrorNotSupported;
+    const cuuint64_t dims[3] = {(cuuint64_t)L.px, (cuuint64_t)(L.pp / L.px), (cuuint64_t)(L.alloc / L.pp)};
+    const cuuint64_t strides[2] = {(cuuint64_t)L.px * sizeof(T), (cuuint64_t)L.pp * sizeof(T)};
+    const cuuint32_t box[3] = {(cuuint32_t)M3<T>::RW, (cuuint32_t)box_rows, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                    const_cast<T*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <class T, int S, bool FZ>
+cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
+                                 T omega, cudaStream_t s) {
+    using G = M3<T>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_sweep3d_march<T, S, FZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)G::smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    // base pointers of the allocations (the layout origin is an offset into them)
+    const T* xbase = x ? x : b;  // FZ never reads x; any valid map works
+    CUtensorMap xm, bm;
+    cudaError_t e = make_map<T>(&xm, L, xbase, G::XR);
+    if (e != cudaSuccess) return e;
+    e = make_map<T>(&bm, L, b, G::BR);
+    if (e != cudaSuccess) return e;
+    static int occ = 0;
+    if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep3d_march<T, S, FZ>, M3_THREADS, G::smem);
+        if (occ <= 0) occ = 1;
+    }
+    const int tx = (L.n + G::TX - 1) / G::TX, ty = (L.n + G::TY - 1) / G::TY;
+    const int slots = num_sms() * occ;
+    int chunks = std::max(1, (int)((2LL * slots + tx * ty - 1) / (tx * ty)));  // ~2 waves of marching CTAs
+    int planes = (L.n + chunks - 1) / chunks;
+    if (planes < 8) planes = 8;
+    chunks = (L.n + planes - 1) / planes;
+    dim3 g(tx, ty, chunks);
+    k_sweep3d_march<T, S, FZ><<<g, M3_THREADS, G::smem, s>>>(L, xm, bm, x, xo, M, sA, sM, omega, planes);
+    return cudaGetLastError();
+}
+
+#define SPAIMG_M3_INST(T, S)                                                                                       \
+    template cudaError_t launch_sweep3d_march<T, S, false>(const Layout&, const T*, const T*, T*, const Terms<T>&, \
+                                                           T, T, T, cudaStream_t);                               \
+    template cudaError_t launch_sweep3d_march<T, S, true>(const Layout&, const T*, const T*, T*, const Terms<T>&,  \
+                                                          T, T, T, cudaStream_t);
+SPAIMG_M3_INST(double, SHAPE_GENERIC)
+SPAIMG_M3_INST(double, SHAPE_C1)
+SPAIMG_M3_INST(double, SHAPE_STAR7)
+SPAIMG_M3_INST(float, SHAPE_GENERIC)
+SPAIMG_M3_INST(float, SHAPE_C1)
+SPAIMG_M3_INST(float, SHAPE_STAR7)
+
+}  // namespace spaimg

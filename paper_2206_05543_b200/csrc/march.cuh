@@ -1,0 +1,68 @@
+// Helpers shared by the marching kernels (K1 sweep, K2 residual+restriction).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "spaimg_common.cuh"
+
+namespace spaimg {
+
+template <class T, int S>
+__device__ __forceinline__ int toff(const Terms<T>& M, int k, int a) {
+    if constexpr (S == SHAPE_GENERIC) {
+        return M.off[k][a];
+    } else {
+        return ShapeT<S>::o(k, a);
+    }
+}
+template <class T, int S>
+__device__ __forceinline__ int tnt(const Terms<T>& M) {
+    if constexpr (S == SHAPE_GENERIC) {
+        return M.nt;
+    } else {
+        return ShapeT<S>::nt;
+    }
+}
+
+template <class T> struct V16;
+template <> struct V16<double> {
+    using type = double2;
+    static __device__ __forceinline__ void ld(const double* p, double* v) {
+        const double2 t = *reinterpret_cast<const double2*>(p);
+        v[0] = t.x;
+        v[1] = t.y;
+    }
+    static __device__ __forceinline__ void st(double* p, const double* v) {
+        *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+    }
+};
+template <> struct V16<float> {
+    using type = float4;
+    static __device__ __forceinline__ void ld(const float* p, float* v) {
+        const float4 t = *reinterpret_cast<const float4*>(p);
+        v[0] = t.x;
+        v[1] = t.y;
+        v[2] = t.z;
+        v[3] = t.w;
+    }
+    static __device__ __forceinline__ void st(float* p, const float* v) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+};
+
+// streaming 16-byte global store that does not allocate in L1
+template <class T>
+__device__ __forceinline__ void stg16(T* p, const T* v) { V16<T>::st(p, v); }
+
+inline int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+}  // namespace spaimg

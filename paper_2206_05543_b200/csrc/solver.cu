@@ -413,6 +413,7 @@ template <class T> struct Solver final : spaimg_solver {
     ~Solver() override {
         for (int i = 0; i < 2; ++i)
             if (exec[i]) cudaGraphExecDestroy(exec[i]);
+        for (auto& kv : op_graphs) cudaGraphExecDestroy(kv.second);
         for (void* p : owned) cudaFree(p);
         if (norms_h) cudaFreeHost(norms_h);
     }
@@ -631,28 +632,47 @@ template <class T> struct Solver final : spaimg_solver {
         return store_dense<T>(sc, lv[0].L, lv[0].x[cur], out, s, stage);
     }
 
-    int op(int which, int reps, cudaStream_t s) override {
+    int op_launch(int which, cudaStream_t s) {
         Level<T>& L = lv[0];
-        for (int k = 0; k < reps; ++k) {
-            switch (which) {
-                case 0:
-                    if (nsmooth() < 1) return fail(SPAIMG_EINVAL, "no smoothing level");
-                    if (int rc = do_sweep<T>(L, cur, false, M, shape, fused, omega, s, nullptr)) return rc;
-                    break;
-                case 1:
-                    if (nsmooth() < 1) return fail(SPAIMG_EINVAL, "no coarse level");
-                    CK(launch_residual_restrict<T>(L.L, lv[1].L, L.x[cur], L.b, lv[1].b, L.sA, L.r, s));
-                    break;
-                case 2:
-                    if (nsmooth() < 1) return fail(SPAIMG_EINVAL, "no coarse level");
-                    CK(launch_prolong_correct<T>(L.L, lv[1].L, L.x[1 - cur], lv[1].x[0], s));
-                    break;
-                case 3:
-                    CK(launch_residual_norm<T>(L.L, L.x[cur], L.b, L.sA, partials, counter, norms_d, 0, nullptr, s));
-                    break;
-                default: return fail(SPAIMG_EINVAL, "unknown op");
-            }
+        if (nsmooth() < 1) return fail(SPAIMG_EINVAL, "no smoothing level");
+        switch (which) {
+            case 0: return do_sweep<T>(L, cur, false, M, shape, fused, omega, s, nullptr);
+            case 1: CK(launch_residual_restrict<T>(L.L, lv[1].L, L.x[cur], L.b, lv[1].b, L.sA, L.r, s)); return 0;
+            case 2: CK(launch_prolong_correct<T>(L.L, lv[1].L, L.x[1 - cur], lv[1].x[0], s)); return 0;
+            case 3:
+                CK(launch_residual_norm<T>(L.L, L.x[cur], L.b, L.sA, partials, counter, norms_d, 0, nullptr, s));
+                return 0;
+            default: return fail(SPAIMG_EINVAL, "unknown op");
         }
+    }
+
+    // `reps` back-to-back launches of one kernel, replayed from a cached CUDA graph so the
+    // per-launch time excludes host launch gaps (used for per-operator timing)
+    std::vector<std::pair<long long, cudaGraphExec_t>> op_graphs;
+    int op(int which, int reps, cudaStream_t s) override {
+        if (reps <= 1) return reps == 1 ? op_launch(which, s) : 0;
+        const long long key = ((long long)which * 1000003 + reps) * 2 + cur;
+        for (auto& kv : op_graphs)
+            if (kv.first == key) {
+                CK(cudaGraphLaunch(kv.second, s));
+                return 0;
+            }
+        cudaStream_t cs;
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        int rc = 0;
+        for (int k = 0; k < reps && !rc; ++k) rc = op_launch(which, cs);
+        cudaError_t e = cudaStreamEndCapture(cs, &g);
+        cudaStreamDestroy(cs);
+        if (rc) return rc;
+        if (e != cudaSuccess) return fail((int)e, "op capture failed");
+        cudaGraphExec_t ex;
+        e = cudaGraphInstantiate(&ex, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail((int)e, "op graph instantiate failed");
+        op_graphs.push_back({key, ex});
+        CK(cudaGraphLaunch(ex, s));
         return 0;
     }
 

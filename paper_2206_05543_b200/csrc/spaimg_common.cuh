@@ -52,7 +52,7 @@ struct Layout {
 
 // tile extents the layout guarantees as addressable slack past the interior
 constexpr int kTileX2D = 512;   // widest 2D strip (columns)
-constexpr int kTileX3D = 64;    // widest 3D tile (columns)
+constexpr int kTileX3D = 128;   // widest 3D tile (columns)
 constexpr int kTileY3D = 32;    // tallest 3D tile (rows)
 constexpr int kGhost = 2;       // ghost rows/planes on the marching axes
 
