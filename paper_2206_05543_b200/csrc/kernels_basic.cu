@@ -8,6 +8,7 @@
 #include <cmath>
 
 #include "kernels.h"
+#include "march.cuh"
 
 namespace spaimg {
 
@@ -222,74 +223,137 @@ cudaError_t launch_restrict(const Layout& Lf, const Layout& Lc, const T* r, T* b
 // ------------------------------------------------------------------------------------------
 // K3: prolongation + correction, in place (multigrid.py:122-144, :184)
 // ------------------------------------------------------------------------------------------
+// One thread per coarse cell (I, J[, K]) produces the 2^d fine points (2I..2I+1, 2J..2J+1, ...)
+// it owns (cells on the far side own only the fine points that exist).  The separable passes
+// run axis 0 first exactly as the reference (axis-0 interpolants t, then axis 1 [, axis 2]);
+// coarse values at J-1 / K-1 come from the neighbouring lane by shuffle, the zero frame of the
+// coarse level supplies the boundary zeros, and the first/last flags keep the reference's
+// 0.5*a[0] / 0.5*a[-1] end formulas bit for bit.  Fine rows move as 16-byte vectors.
 template <class T>
-__device__ __forceinline__ T pline(T am1, T a0, int i, int m) {
-    // value at fine index i given a0 = a[i>>1] (odd) or am1 = a[j-1], a0 = a[j] (even i = 2j)
-    if (i & 1) return a0;
-    const int j = i >> 1;
-    return pl_even<T>(am1, a0, j == 0, j == m);
+__device__ __forceinline__ T pe(T am1, T a0, bool first, bool last) {
+    return pl_even<T>(am1, a0, first, last);
 }
 
 template <class T>
-__device__ __forceinline__ T cval(const Layout& Lc, const T* e, int I, int J, int K) {
-    // coarse value with the frame: indices in [-1, m] read zero outside the interior
-    return e[pidx(Lc, I, J, K)];
-}
-
-template <class T>
-__global__ void k_prolong_correct(Layout Lf, Layout Lc, T* __restrict__ x, const T* __restrict__ e, bool acc) {
+__global__ void __launch_bounds__(128) k_prolong_correct2d(Layout Lf, Layout Lc, T* __restrict__ x,
+                                                           const T* __restrict__ e, bool acc) {
     using O = Op<T>;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= Lf.n) return;
     const int m = Lc.n;
-    if (Lf.dim == 2) {
-        const int i = blockIdx.y, j = k;
-        // axis 0 first: t[i, J] for the coarse columns J the axis-1 pass needs
-        const int J1 = j >> 1, J0 = (j & 1) ? J1 : J1 - 1;  // even j=2J needs J-1, J; odd needs J
-        auto t_at = [&](int J) -> T {
-            const int I1 = i >> 1;
-            if (i & 1) return cval(Lc, e, I1, J, 0);
-            return pl_even<T>(I1 > 0 ? cval(Lc, e, I1 - 1, J, 0) : T(0), I1 < m ? cval(Lc, e, I1, J, 0) : T(0),
-                              I1 == 0, I1 == m);
-        };
-        T v;
-        if (j & 1) {
-            v = t_at(J1);
+    const int J = blockIdx.x * blockDim.x + threadIdx.x;
+    const int I = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    // coarse values at rows I-1, I (frame rows are zero) and columns J, J-1
+    const T* ec = e + Lc.origin + (long long)I * Lc.px + J;
+    const T e10 = ec[-Lc.px], e11 = ec[0];           // (I-1, J), (I, J)
+    T e00 = __shfl_up_sync(0xffffffffu, e10, 1);     // (I-1, J-1)
+    T e01 = __shfl_up_sync(0xffffffffu, e11, 1);     // (I, J-1)
+    if (lane == 0) {
+        e00 = ec[-Lc.px - 1];
+        e01 = ec[-1];
+    }
+    if (J > m) return;
+    const bool fI = I == 0, lI = I == m, fJ = J == 0, lJ = J == m;
+    // axis 0: interpolants at fine rows 2I (even) and 2I+1 (odd) for coarse columns J-1, J
+    const T te0 = pe<T>(e00, e01, fI, lI), te1 = pe<T>(e10, e11, fI, lI);  // row 2I
+    const T to0 = e01, to1 = e11;                                           // row 2I+1
+    T* row0 = x + Lf.origin + (long long)(2 * I) * Lf.px + 2 * J;
+    const int nf = Lf.n;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (2 * I + h >= nf) break;
+        const T a0 = h ? to0 : te0, a1 = h ? to1 : te1;
+        T v[2];
+        v[0] = pe<T>(a0, a1, fJ, lJ);  // column 2J
+        v[1] = a1;                     // column 2J+1
+        T* p = row0 + (long long)h * Lf.px;
+        if (!lJ) {
+            T o[2];
+            if (acc) {
+                V16<T>::ld2(p, o);
+                o[0] = O::add(o[0], v[0]);
+                o[1] = O::add(o[1], v[1]);
+            } else {
+                o[0] = v[0];
+                o[1] = v[1];
+            }
+            V16<T>::st2(p, o);
         } else {
-            const T a0 = J1 < m ? t_at(J1) : T(0);
-            const T am1 = J1 > 0 ? t_at(J0) : T(0);
-            v = pl_even<T>(am1, a0, J1 == 0, J1 == m);
+            p[0] = acc ? O::add(p[0], v[0]) : v[0];
         }
-        const long long p = pidx(Lf, i, j, 0);
-        x[p] = acc ? O::add(x[p], v) : v;
-    } else {
-        const int i = blockIdx.z, j = blockIdx.y;
-        auto t_at = [&](int J, int K) -> T {  // axis-0 pass at fine plane i, coarse (J, K)
-            const int I1 = i >> 1;
-            if (i & 1) return cval(Lc, e, I1, J, K);
-            return pl_even<T>(I1 > 0 ? cval(Lc, e, I1 - 1, J, K) : T(0), I1 < m ? cval(Lc, e, I1, J, K) : T(0),
-                              I1 == 0, I1 == m);
-        };
-        auto u_at = [&](int K) -> T {  // axis-1 pass at fine (i, j), coarse K
-            const int J1 = j >> 1;
-            if (j & 1) return t_at(J1, K);
-            return pl_even<T>(J1 > 0 ? t_at(J1 - 1, K) : T(0), J1 < m ? t_at(J1, K) : T(0), J1 == 0, J1 == m);
-        };
-        const int K1 = k >> 1;
-        T v;
-        if (k & 1) {
-            v = u_at(K1);
-        } else {
-            v = pl_even<T>(K1 > 0 ? u_at(K1 - 1) : T(0), K1 < m ? u_at(K1) : T(0), K1 == 0, K1 == m);
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(128) k_prolong_correct3d(Layout Lf, Layout Lc, T* __restrict__ x,
+                                                           const T* __restrict__ e, bool acc) {
+    using O = Op<T>;
+    const int m = Lc.n;
+    const int K = blockIdx.x * blockDim.x + threadIdx.x;
+    const int J = blockIdx.y, I = blockIdx.z;
+    const int lane = threadIdx.x & 31;
+    // c[di][dj][dk]: coarse value at (I-1+di, J-1+dj, K-1+dk)
+    T c[2][2][2];
+    const T* ec = e + Lc.origin + (long long)I * Lc.pp + (long long)J * Lc.px + K;
+#pragma unroll
+    for (int di = 0; di < 2; ++di)
+#pragma unroll
+        for (int dj = 0; dj < 2; ++dj) {
+            const T* q = ec + (long long)(di - 1) * Lc.pp + (long long)(dj - 1) * Lc.px;
+            c[di][dj][1] = q[0];
+            c[di][dj][0] = __shfl_up_sync(0xffffffffu, c[di][dj][1], 1);
+            if (lane == 0) c[di][dj][0] = q[-1];
         }
-        const long long p = pidx(Lf, i, j, k);
-        x[p] = acc ? O::add(x[p], v) : v;
+    if (K > m) return;
+    const bool fI = I == 0, lI = I == m, fJ = J == 0, lJ = J == m, fK = K == 0, lK = K == m;
+    const int nf = Lf.n;
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi) {
+        if (2 * I + hi >= nf) break;
+        // axis 0 at fine plane 2I+hi, coarse (J-1+dj, K-1+dk)
+        T t[2][2];
+#pragma unroll
+        for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+            for (int dk = 0; dk < 2; ++dk) t[dj][dk] = hi ? c[1][dj][dk] : pe<T>(c[0][dj][dk], c[1][dj][dk], fI, lI);
+#pragma unroll
+        for (int hj = 0; hj < 2; ++hj) {
+            if (2 * J + hj >= nf) break;
+            // axis 1 at fine row 2J+hj, coarse K-1+dk
+            T u[2];
+#pragma unroll
+            for (int dk = 0; dk < 2; ++dk) u[dk] = hj ? t[1][dk] : pe<T>(t[0][dk], t[1][dk], fJ, lJ);
+            T v[2];
+            v[0] = pe<T>(u[0], u[1], fK, lK);  // column 2K
+            v[1] = u[1];                       // column 2K+1
+            T* p = x + Lf.origin + (long long)(2 * I + hi) * Lf.pp + (long long)(2 * J + hj) * Lf.px + 2 * K;
+            if (!lK) {
+                T o[2];
+                if (acc) {
+                    V16<T>::ld2(p, o);
+                    o[0] = O::add(o[0], v[0]);
+                    o[1] = O::add(o[1], v[1]);
+                } else {
+                    o[0] = v[0];
+                    o[1] = v[1];
+                }
+                V16<T>::st2(p, o);
+            } else {
+                p[0] = acc ? O::add(p[0], v[0]) : v[0];
+            }
+        }
     }
 }
 
 template <class T>
 cudaError_t launch_prolong_correct(const Layout& Lf, const Layout& Lc, T* x, const T* e, cudaStream_t s, bool acc) {
-    k_prolong_correct<T><<<pgrid(Lf, 128), 128, 0, s>>>(Lf, Lc, x, e, acc);
+    const int m = Lc.n;
+    if (Lf.dim == 2) {
+        dim3 g((m + 1 + 127) / 128, m + 1);
+        k_prolong_correct2d<T><<<g, 128, 0, s>>>(Lf, Lc, x, e, acc);
+    } else {
+        dim3 g((m + 1 + 127) / 128, m + 1, m + 1);
+        k_prolong_correct3d<T><<<g, 128, 0, s>>>(Lf, Lc, x, e, acc);
+    }
     return cudaGetLastError();
 }
 

@@ -395,8 +395,14 @@ cudaError_t launch_sweep(const Layout& L, const T* x, const T* b, T* xo, const T
 // K2 v1: residual into scratch, then restriction
 // ------------------------------------------------------------------------------------------
 template <class T>
+cudaError_t launch_residual_restrict2d_march(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T sA,
+                                             cudaStream_t s);
+
+template <class T>
 cudaError_t launch_residual_restrict(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T sA,
                                      T* scratch_r, cudaStream_t s) {
+    if (Lf.dim == 2 && !getenv("SPAIMG_RESTRICT_V1"))
+        return launch_residual_restrict2d_march<T>(Lf, Lc, x, b, bc, sA, s);
     cudaError_t e = launch_residual<T>(Lf, x, b, scratch_r, sA, s);
     if (e != cudaSuccess) return e;
     return launch_restrict<T>(Lf, Lc, scratch_r, bc, s);

@@ -35,6 +35,9 @@ template <> struct V16<double> {
     static __device__ __forceinline__ void st(double* p, const double* v) {
         *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
     }
+    // two consecutive elements (16 B for double)
+    static __device__ __forceinline__ void ld2(const double* p, double* v) { ld(p, v); }
+    static __device__ __forceinline__ void st2(double* p, const double* v) { st(p, v); }
 };
 template <> struct V16<float> {
     using type = float4;
@@ -47,6 +50,15 @@ template <> struct V16<float> {
     }
     static __device__ __forceinline__ void st(float* p, const float* v) {
         *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    // two consecutive elements (8 B for float)
+    static __device__ __forceinline__ void ld2(const float* p, float* v) {
+        const float2 t = *reinterpret_cast<const float2*>(p);
+        v[0] = t.x;
+        v[1] = t.y;
+    }
+    static __device__ __forceinline__ void st2(float* p, const float* v) {
+        *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
     }
 };
 

@@ -185,6 +185,9 @@ static int alloc_level(Scratch& sc, Level<T>& lv, int dim, int N, bool two_x, bo
     return 0;
 }
 
+// kernel launches of one residual+restriction (2D: one fused marching kernel)
+static int residual_restrict_launches(int dim) { return dim == 2 && !getenv("SPAIMG_RESTRICT_V1") ? 1 : 2; }
+
 // one smoothing step on a level: x[a] -> x[1-a]
 template <class T>
 static int do_sweep(Level<T>& lv, int a, bool fz, const Terms<T>& M, int shape, bool fused, T omega, cudaStream_t s,
@@ -499,7 +502,7 @@ template <class T> struct Solver final : spaimg_solver {
         }
         Level<T>& C = lv[l + 1];
         if (launch_residual_restrict<T>(L.L, C.L, L.x[a], L.b, C.b, L.sA, L.r, s) != cudaSuccess) return -1;
-        *launches += 2;
+        *launches += residual_restrict_launches(cfg.dim);
         int c;
         if (l + 1 == nsmooth()) {
             if (launch_coarse_solve<T>(C.L, C.b, C.x[0], lu, piv, nlu, s) != cudaSuccess) return -1;
