@@ -310,7 +310,8 @@ def run_ours(args):
     h2d = b.nbytes
     d2h = b.nbytes + 8 * (k_e + 1)
 
-    launches = int(args.steps * (1 + cycles_per_step * stats["kernels_per_cycle"]))
+    stats = solver.stats()
+    launches = int(args.steps * (1 + cycles_per_step * stats["kernels_per_cycle"] + stats["kernels_stop_test"]))
 
     extra = {}
     if not args.no_extra and rank == 0:

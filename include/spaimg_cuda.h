@@ -77,11 +77,14 @@ typedef struct spaimg_solver spaimg_solver;
 
 typedef struct spaimg_solver_stats {
     int levels;              /* smoothing levels (excluding the coarse solve level) */
-    int kernels_per_cycle;   /* kernel launches in one captured cycle (incl. the norm) */
+    int kernels_per_cycle;   /* kernel launches per cycle of the device-side solve loop (incl. norm + stop test) */
     double bytes_per_cycle;  /* SURVEY.md §8d minimal algorithmic bytes of one cycle + norm */
     long long unknowns;      /* (N-1)^dim on the finest level */
     int graph;               /* 1 if cycles replay a CUDA graph */
     int fused_sweep;         /* 1 if the fused K1 sweep is used for this smoother */
+    int kernels_stop_test;   /* launches of the per-cycle norm + stop-test part (also run once
+                                more after the last cycle): a solve of K cycles launches
+                                1 + K*kernels_per_cycle + kernels_stop_test kernels */
 } spaimg_solver_stats;
 
 SPAIMG_API const char *spaimg_last_error(void);

@@ -51,6 +51,7 @@ class SpaimgSolverStats(ctypes.Structure):
         ("unknowns", ctypes.c_longlong),
         ("graph", ctypes.c_int),
         ("fused_sweep", ctypes.c_int),
+        ("kernels_stop_test", ctypes.c_int),
     ]
 
 

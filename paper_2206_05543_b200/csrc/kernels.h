@@ -28,18 +28,23 @@ template <class T>
 cudaError_t launch_restrict(const Layout& Lf, const Layout& Lc, const T* r, T* bc, cudaStream_t s);
 
 // K1: fused smoothing sweep x' = x + omega M (b - A x); from_zero => x == 0 (x not read)
+// no != nullptr additionally appends ||b - A x|| (of the INPUT x) to the device history.
 template <class T>
 cudaError_t launch_sweep(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, int shape, T sA,
-                         T sM, T omega, bool from_zero, cudaStream_t s);
+                         T sM, T omega, bool from_zero, cudaStream_t s, const NormOut* no = nullptr);
 bool sweep_fused_supported(int dim, int shape);
+bool sweep_norm_supported();
+// K4 through the marching kernels: ||b - A x|| appended to the device history
+template <class T>
+cudaError_t launch_norm_march(const Layout& L, const T* x, const T* b, T sA, const NormOut& no, cudaStream_t s);
 
 // K2: fused residual + full-weighting restriction
 template <class T>
 cudaError_t launch_residual_restrict(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T sA,
                                      T* scratch_r, cudaStream_t s);
-// K3: fused prolongation + correction (in place on x); acc=false stores prolong(e) alone
+// K3: fused prolongation + correction xo = xi + P e (xi == xo allowed); acc=false stores P e alone
 template <class T>
-cudaError_t launch_prolong_correct(const Layout& Lf, const Layout& Lc, T* x, const T* e, cudaStream_t s,
+cudaError_t launch_prolong_correct(const Layout& Lf, const Layout& Lc, const T* xi, T* xo, const T* e, cudaStream_t s,
                                    bool acc = true);
 
 // K4: deterministic two-stage ||b - A x||_2 into norms[slot] (double); partials/counter scratch

@@ -235,7 +235,7 @@ __device__ __forceinline__ T pe(T am1, T a0, bool first, bool last) {
 }
 
 template <class T>
-__global__ void __launch_bounds__(128) k_prolong_correct2d(Layout Lf, Layout Lc, T* __restrict__ x,
+__global__ void __launch_bounds__(128) k_prolong_correct2d(Layout Lf, Layout Lc, const T* xi, T* xo,
                                                            const T* __restrict__ e, bool acc) {
     using O = Op<T>;
     const int m = Lc.n;
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(128) k_prolong_correct2d(Layout Lf, Layout Lc,
     // axis 0: interpolants at fine rows 2I (even) and 2I+1 (odd) for coarse columns J-1, J
     const T te0 = pe<T>(e00, e01, fI, lI), te1 = pe<T>(e10, e11, fI, lI);  // row 2I
     const T to0 = e01, to1 = e11;                                           // row 2I+1
-    T* row0 = x + Lf.origin + (long long)(2 * I) * Lf.px + 2 * J;
+    const long long off0 = Lf.origin + (long long)(2 * I) * Lf.px + 2 * J;
     const int nf = Lf.n;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -265,26 +265,26 @@ __global__ void __launch_bounds__(128) k_prolong_correct2d(Layout Lf, Layout Lc,
         T v[2];
         v[0] = pe<T>(a0, a1, fJ, lJ);  // column 2J
         v[1] = a1;                     // column 2J+1
-        T* p = row0 + (long long)h * Lf.px;
+        const long long off = off0 + (long long)h * Lf.px;
         if (!lJ) {
             T o[2];
             if (acc) {
-                V16<T>::ld2(p, o);
+                V16<T>::ld2(xi + off, o);
                 o[0] = O::add(o[0], v[0]);
                 o[1] = O::add(o[1], v[1]);
             } else {
                 o[0] = v[0];
                 o[1] = v[1];
             }
-            V16<T>::st2(p, o);
+            V16<T>::st2(xo + off, o);
         } else {
-            p[0] = acc ? O::add(p[0], v[0]) : v[0];
+            xo[off] = acc ? O::add(xi[off], v[0]) : v[0];
         }
     }
 }
 
 template <class T>
-__global__ void __launch_bounds__(128) k_prolong_correct3d(Layout Lf, Layout Lc, T* __restrict__ x,
+__global__ void __launch_bounds__(128) k_prolong_correct3d(Layout Lf, Layout Lc, const T* xi, T* xo,
                                                            const T* __restrict__ e, bool acc) {
     using O = Op<T>;
     const int m = Lc.n;
@@ -325,34 +325,35 @@ __global__ void __launch_bounds__(128) k_prolong_correct3d(Layout Lf, Layout Lc,
             T v[2];
             v[0] = pe<T>(u[0], u[1], fK, lK);  // column 2K
             v[1] = u[1];                       // column 2K+1
-            T* p = x + Lf.origin + (long long)(2 * I + hi) * Lf.pp + (long long)(2 * J + hj) * Lf.px + 2 * K;
+            const long long off = Lf.origin + (long long)(2 * I + hi) * Lf.pp + (long long)(2 * J + hj) * Lf.px + 2 * K;
             if (!lK) {
                 T o[2];
                 if (acc) {
-                    V16<T>::ld2(p, o);
+                    V16<T>::ld2(xi + off, o);
                     o[0] = O::add(o[0], v[0]);
                     o[1] = O::add(o[1], v[1]);
                 } else {
                     o[0] = v[0];
                     o[1] = v[1];
                 }
-                V16<T>::st2(p, o);
+                V16<T>::st2(xo + off, o);
             } else {
-                p[0] = acc ? O::add(p[0], v[0]) : v[0];
+                xo[off] = acc ? O::add(xi[off], v[0]) : v[0];
             }
         }
     }
 }
 
 template <class T>
-cudaError_t launch_prolong_correct(const Layout& Lf, const Layout& Lc, T* x, const T* e, cudaStream_t s, bool acc) {
+cudaError_t launch_prolong_correct(const Layout& Lf, const Layout& Lc, const T* xi, T* xo, const T* e, cudaStream_t s,
+                                   bool acc) {
     const int m = Lc.n;
     if (Lf.dim == 2) {
         dim3 g((m + 1 + 127) / 128, m + 1);
-        k_prolong_correct2d<T><<<g, 128, 0, s>>>(Lf, Lc, x, e, acc);
+        k_prolong_correct2d<T><<<g, 128, 0, s>>>(Lf, Lc, xi, xo, e, acc);
     } else {
         dim3 g((m + 1 + 127) / 128, m + 1, m + 1);
-        k_prolong_correct3d<T><<<g, 128, 0, s>>>(Lf, Lc, x, e, acc);
+        k_prolong_correct3d<T><<<g, 128, 0, s>>>(Lf, Lc, xi, xo, e, acc);
     }
     return cudaGetLastError();
 }
@@ -506,7 +507,7 @@ cudaError_t launch_coarse_solve(const Layout& L, const T* b, T* x, const T* lu, 
     template cudaError_t launch_relax<T>(const Layout&, const T*, const T*, T*, const Terms<T>&, int, T, T,     \
                                          cudaStream_t);                                                         \
     template cudaError_t launch_restrict<T>(const Layout&, const Layout&, const T*, T*, cudaStream_t);          \
-    template cudaError_t launch_prolong_correct<T>(const Layout&, const Layout&, T*, const T*, cudaStream_t, bool);\
+    template cudaError_t launch_prolong_correct<T>(const Layout&, const Layout&, const T*, T*, const T*, cudaStream_t, bool); \
     template cudaError_t launch_residual_norm<T>(const Layout&, const T*, const T*, T, double*, unsigned*,      \
                                                  double*, int, int*, cudaStream_t);                             \
     template cudaError_t launch_coarse_solve<T>(const Layout&, const T*, T*, const T*, const int*, int,         \

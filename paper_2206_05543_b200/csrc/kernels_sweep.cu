@@ -147,7 +147,7 @@ struct M2Ctx {
     const T* brow0;
     T* orow0;  // output row 0, own first column
     long long px;
-    int n, c0, col, sidx, q0, q_last, r0, lane;
+    int n, c0, col, sidx, q0, q_last, r0, r_end, lane;
     bool producer, last_strip;
 };
 
@@ -163,9 +163,10 @@ __device__ __forceinline__ void m2_issue(const M2Ctx<T>& c, int q, int slot) {
 
 // One marching step k (row j = q0 + k): r(j) for the strip (+ halo), then output row j-1.
 // P = k mod 6 makes every stage slot and register-row index a compile-time constant.
-template <class T, int S, bool FZ, int P>
+template <class T, int S, bool FZ, int NM, int P>
 __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_vec<T>()], T (&R)[3][m2_vec<T>()],
-                                        T (&RL)[3], T (&RH)[3], const Terms<T>& M, T sA, T sM, T omega) {
+                                        T (&RL)[3], T (&RH)[3], const Terms<T>& M, T sA, T sM, T omega,
+                                        double& nacc) {
     using O = Op<T>;
     constexpr int VEC = m2_vec<T>();
     constexpr int W = m2_width<T>();
@@ -200,8 +201,12 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
             for (int v = 0; v < VEC; ++v)
                 if (!row_in || c.col + v >= c.n) R[ic][v] = T(0);  // r is zero outside the interior
         }
-        V16<T>::st(rrow + c.sidx, R[ic]);
-    } else if (c.lane < 2) {
+        if (NM && j >= c.r0 && j < c.r_end) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) nacc += (double)R[ic][v] * (double)R[ic][v];  // ||r||^2, own rows
+        }
+        if (NM != 2) V16<T>::st(rrow + c.sidx, R[ic]);
+    } else if (NM != 2 && c.lane < 2) {
         // strip-halo residuals at columns c0-1 (lane 0) and c0+W (lane 1)
         const int si = c.lane == 0 ? VEC - 1 : VEC + W;
         const int cc = c.lane == 0 ? c.c0 - 1 : c.c0 + W;
@@ -221,6 +226,7 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
         if (c.lane == 0 && j - 1 + ST <= c.q_last) m2_issue<T, S, FZ>(c, j - 1 + ST, sm);
         return;
     }
+    if (NM == 2) return;
     RL[ic] = rrow[c.sidx - 1];
     RH[ic] = rrow[c.sidx + VEC];
     if (j - 1 < c.r0) return;
@@ -249,10 +255,11 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
     }
 }
 
-template <class T, int S, bool FZ>
+template <class T, int S, bool FZ, int NM>
 __global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, const T* __restrict__ x,
                                                                      const T* __restrict__ b, T* __restrict__ xo,
-                                                                     Terms<T> M, T sA, T sM, T omega, int rows) {
+                                                                     Terms<T> M, T sA, T sM, T omega, int rows,
+                                                                     NormOut no) {
     constexpr int VEC = m2_vec<T>();
     constexpr int W = m2_width<T>();
     constexpr int RW = m2_rowlen<T>();
@@ -271,6 +278,7 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, co
     c.c0 = blockIdx.x * W;
     c.r0 = blockIdx.y * rows;
     const int r_end = min(c.r0 + rows, c.n);
+    c.r_end = r_end;
     c.q0 = c.r0 - 2;        // first staged row
     c.q_last = r_end + 1;   // last staged row
     c.last_strip = c.c0 + W > c.n;
@@ -301,25 +309,27 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, co
         V16<T>::ld(c.xs + 0 * RW + c.sidx, X[0]);  // x(q0)   = x(j-1) of step k = 1
         V16<T>::ld(c.xs + 1 * RW + c.sidx, X[1]);  // x(q0+1) = x(j)
     }
+    double nacc = 0.0;
     const int K = r_end - c.q0;  // steps k = 1 .. K  (rows j = r0-1 .. r_end)
     for (int kb = 0; kb <= K; kb += ST) {
-        if (kb >= 1) m2_step<T, S, FZ, 0>(c, kb, X, R, RL, RH, M, sA, sM, omega);
-        if (kb + 1 <= K) m2_step<T, S, FZ, 1>(c, kb + 1, X, R, RL, RH, M, sA, sM, omega);
-        if (kb + 2 <= K) m2_step<T, S, FZ, 2>(c, kb + 2, X, R, RL, RH, M, sA, sM, omega);
-        if (kb + 3 <= K) m2_step<T, S, FZ, 3>(c, kb + 3, X, R, RL, RH, M, sA, sM, omega);
-        if (kb + 4 <= K) m2_step<T, S, FZ, 4>(c, kb + 4, X, R, RL, RH, M, sA, sM, omega);
-        if (kb + 5 <= K) m2_step<T, S, FZ, 5>(c, kb + 5, X, R, RL, RH, M, sA, sM, omega);
+        if (kb >= 1) m2_step<T, S, FZ, NM, 0>(c, kb, X, R, RL, RH, M, sA, sM, omega, nacc);
+        if (kb + 1 <= K) m2_step<T, S, FZ, NM, 1>(c, kb + 1, X, R, RL, RH, M, sA, sM, omega, nacc);
+        if (kb + 2 <= K) m2_step<T, S, FZ, NM, 2>(c, kb + 2, X, R, RL, RH, M, sA, sM, omega, nacc);
+        if (kb + 3 <= K) m2_step<T, S, FZ, NM, 3>(c, kb + 3, X, R, RL, RH, M, sA, sM, omega, nacc);
+        if (kb + 4 <= K) m2_step<T, S, FZ, NM, 4>(c, kb + 4, X, R, RL, RH, M, sA, sM, omega, nacc);
+        if (kb + 5 <= K) m2_step<T, S, FZ, NM, 5>(c, kb + 5, X, R, RL, RH, M, sA, sM, omega, nacc);
     }
+    if (NM) norm_epilogue(nacc, no);
 }
 
-template <class T, int S, bool FZ>
+template <class T, int S, bool FZ, int NM>
 static cudaError_t launch_sweep2d_march(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA,
-                                        T sM, T omega, cudaStream_t s) {
+                                        T sM, T omega, const NormOut& no, cudaStream_t s) {
     constexpr size_t smem = m2_smem_bytes<T>();
     constexpr int threads = (M2_NW + 1) * 32;
     static int occ = 0;
     if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep2d_march<T, S, FZ>, threads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep2d_march<T, S, FZ, NM>, threads, smem);
         if (occ <= 0) occ = 1;
     }
     const int W = m2_width<T>();
@@ -330,7 +340,7 @@ static cudaError_t launch_sweep2d_march(const Layout& L, const T* x, const T* b,
     if (rows < 16) rows = 16;
     chunks = (L.n + rows - 1) / rows;
     dim3 g(strips, chunks);
-    k_sweep2d_march<T, S, FZ><<<g, threads, smem, s>>>(L, x, b, xo, M, sA, sM, omega, rows);
+    k_sweep2d_march<T, S, FZ, NM><<<g, threads, smem, s>>>(L, x, b, xo, M, sA, sM, omega, rows, no);
     return cudaGetLastError();
 }
 
@@ -339,56 +349,69 @@ bool sweep_fused_supported(int dim, int shape) {
     return shape == SHAPE_GENERIC || shape == SHAPE_C1 || shape == SHAPE_STAR7;
 }
 
-template <class T, int S, bool FZ>
+template <class T, int S, bool FZ, int NM>
 cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
-                                 T omega, cudaStream_t s);
+                                 T omega, const NormOut& no, cudaStream_t s);
 
-template <class T, int S, bool FZ>
+static bool sweep_v1() { return getenv("SPAIMG_SWEEP_V1") != nullptr; }
+bool sweep_norm_supported() { return !sweep_v1(); }
+
+template <class T, int S, bool FZ, int NM>
 static cudaError_t sweep_dispatch(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
-                                  T omega, cudaStream_t s) {
+                                  T omega, const NormOut& no, cudaStream_t s) {
+    constexpr int S3 = (S == SHAPE_GENERIC || S == SHAPE_C1 || S == SHAPE_STAR7) ? S : SHAPE_GENERIC;
     if (L.dim == 2) {
-        if (getenv("SPAIMG_SWEEP_V1")) {
+        if (sweep_v1() && NM == 0) {
             dim3 g((L.n + S2_TW - 1) / S2_TW, (L.n + S2_TH - 1) / S2_TH);
             k_sweep2d_tile<T, S, FZ><<<g, 256, 0, s>>>(L, x, b, xo, M, sA, sM, omega);
-        } else {
-            return launch_sweep2d_march<T, S, FZ>(L, x, b, xo, M, sA, sM, omega, s);
+            return cudaGetLastError();
         }
-    } else {
-        if (getenv("SPAIMG_SWEEP_V1") || !(S == SHAPE_GENERIC || S == SHAPE_C1 || S == SHAPE_STAR7)) {
-            dim3 g((L.n + S3_TX - 1) / S3_TX, (L.n + S3_TY - 1) / S3_TY, (L.n + S3_TZ - 1) / S3_TZ);
-            k_sweep3d_tile<T, S, FZ><<<g, 256, 0, s>>>(L, x, b, xo, M, sA, sM, omega);
-        } else {
-            return launch_sweep3d_march<T, (S == SHAPE_GENERIC || S == SHAPE_C1 || S == SHAPE_STAR7) ? S : SHAPE_GENERIC,
-                                        FZ>(L, x, b, xo, M, sA, sM, omega, s);
-        }
+        return launch_sweep2d_march<T, S, FZ, NM>(L, x, b, xo, M, sA, sM, omega, no, s);
     }
-    return cudaGetLastError();
+    if (sweep_v1() && NM == 0) {
+        dim3 g((L.n + S3_TX - 1) / S3_TX, (L.n + S3_TY - 1) / S3_TY, (L.n + S3_TZ - 1) / S3_TZ);
+        k_sweep3d_tile<T, S, FZ><<<g, 256, 0, s>>>(L, x, b, xo, M, sA, sM, omega);
+        return cudaGetLastError();
+    }
+    return launch_sweep3d_march<T, S3, FZ, NM>(L, x, b, xo, M, sA, sM, omega, no, s);
 }
 
 template <class T, int S>
 static cudaError_t sweep_fz(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM, T omega,
-                            bool fz, cudaStream_t s) {
-    return fz ? sweep_dispatch<T, S, true>(L, x, b, xo, M, sA, sM, omega, s)
-              : sweep_dispatch<T, S, false>(L, x, b, xo, M, sA, sM, omega, s);
+                            bool fz, const NormOut* no, cudaStream_t s) {
+    const NormOut n0{};
+    if (no)
+        return fz ? sweep_dispatch<T, S, true, 1>(L, x, b, xo, M, sA, sM, omega, *no, s)
+                  : sweep_dispatch<T, S, false, 1>(L, x, b, xo, M, sA, sM, omega, *no, s);
+    return fz ? sweep_dispatch<T, S, true, 0>(L, x, b, xo, M, sA, sM, omega, n0, s)
+              : sweep_dispatch<T, S, false, 0>(L, x, b, xo, M, sA, sM, omega, n0, s);
 }
 
 template <class T>
 cudaError_t launch_sweep(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, int shape, T sA, T sM,
-                         T omega, bool from_zero, cudaStream_t s) {
+                         T omega, bool from_zero, cudaStream_t s, const NormOut* no) {
     switch (shape) {
-        case SHAPE_C1: return sweep_fz<T, SHAPE_C1>(L, x, b, xo, M, sA, sM, omega, from_zero, s);
+        case SHAPE_C1: return sweep_fz<T, SHAPE_C1>(L, x, b, xo, M, sA, sM, omega, from_zero, no, s);
         case SHAPE_STAR5:
-            if (L.dim == 2) return sweep_fz<T, SHAPE_STAR5>(L, x, b, xo, M, sA, sM, omega, from_zero, s);
+            if (L.dim == 2) return sweep_fz<T, SHAPE_STAR5>(L, x, b, xo, M, sA, sM, omega, from_zero, no, s);
             break;
         case SHAPE_BOX9:
-            if (L.dim == 2) return sweep_fz<T, SHAPE_BOX9>(L, x, b, xo, M, sA, sM, omega, from_zero, s);
+            if (L.dim == 2) return sweep_fz<T, SHAPE_BOX9>(L, x, b, xo, M, sA, sM, omega, from_zero, no, s);
             break;
         case SHAPE_STAR7:
-            if (L.dim == 3) return sweep_fz<T, SHAPE_STAR7>(L, x, b, xo, M, sA, sM, omega, from_zero, s);
+            if (L.dim == 3) return sweep_fz<T, SHAPE_STAR7>(L, x, b, xo, M, sA, sM, omega, from_zero, no, s);
             break;
         default: break;
     }
-    return sweep_fz<T, SHAPE_GENERIC>(L, x, b, xo, M, sA, sM, omega, from_zero, s);
+    return sweep_fz<T, SHAPE_GENERIC>(L, x, b, xo, M, sA, sM, omega, from_zero, no, s);
+}
+
+// residual norm alone through the marching machinery (no smoothing output)
+template <class T>
+cudaError_t launch_norm_march(const Layout& L, const T* x, const T* b, T sA, const NormOut& no, cudaStream_t s) {
+    const Terms<T> none{};
+    if (L.dim == 2) return launch_sweep2d_march<T, SHAPE_C1, false, 2>(L, x, b, nullptr, none, sA, T(0), T(0), no, s);
+    return launch_sweep3d_march<T, SHAPE_C1, false, 2>(L, x, b, nullptr, none, sA, T(0), T(0), no, s);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -409,9 +432,13 @@ cudaError_t launch_residual_restrict(const Layout& Lf, const Layout& Lc, const T
 }
 
 template cudaError_t launch_sweep<double>(const Layout&, const double*, const double*, double*, const Terms<double>&,
-                                          int, double, double, double, bool, cudaStream_t);
+                                          int, double, double, double, bool, cudaStream_t, const NormOut*);
 template cudaError_t launch_sweep<float>(const Layout&, const float*, const float*, float*, const Terms<float>&, int,
-                                         float, float, float, bool, cudaStream_t);
+                                         float, float, float, bool, cudaStream_t, const NormOut*);
+template cudaError_t launch_norm_march<double>(const Layout&, const double*, const double*, double, const NormOut&,
+                                               cudaStream_t);
+template cudaError_t launch_norm_march<float>(const Layout&, const float*, const float*, float, const NormOut&,
+                                              cudaStream_t);
 template cudaError_t launch_residual_restrict<double>(const Layout&, const Layout&, const double*, const double*,
                                                       double*, double, double*, cudaStream_t);
 template cudaError_t launch_residual_restrict<float>(const Layout&, const Layout&, const float*, const float*, float*,

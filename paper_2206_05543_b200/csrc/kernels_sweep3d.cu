@@ -51,7 +51,7 @@ struct M3Ctx {
     uint64_t* full;
     T* obase;  // output at (plane 0, own row 0, own column)
     long long px, pp;
-    int n, x0, y0, q0, q_last, z0, yl, xl, tid;
+    int n, x0, y0, q0, q_last, z0, z_end, yl, xl, tid;
     bool edge;  // tile touches the right/bottom boundary (masking needed)
     int cx, cy;  // TMA coordinates of the tile's stage origin (x stage)
 };
@@ -84,10 +84,10 @@ __device__ __forceinline__ T m3_ring_r(const M3Ctx<T>& c, int sj, int sp, int sm
     }
 }
 
-template <class T, int S, bool FZ, int P>
+template <class T, int S, bool FZ, int NM, int P>
 __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xmap, const CUtensorMap* bmap, int k,
                                         T (&X)[3][2][M3<T>::VEC], T (&R)[3][2][M3<T>::VEC], const Terms<T>& M,
-                                        T sA, T sM, T omega) {
+                                        T sA, T sM, T omega, double& nacc) {
     using G = M3<T>;
     using O = Op<T>;
     constexpr int VEC = G::VEC;
@@ -137,10 +137,14 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
             for (int v = 0; v < VEC; ++v)
                 if (!plane_in || c.y0 + row >= c.n || c.x0 + c.xl + v >= c.n) R[ic][yy][v] = T(0);
         }
-        V16<T>::st(rpl + (row + 1) * RW + VEC + c.xl, R[ic][yy]);
+        if (NM && j >= c.z0 && j < c.z_end) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) nacc += (double)R[ic][yy][v] * (double)R[ic][yy][v];
+        }
+        if (NM != 2) V16<T>::st(rpl + (row + 1) * RW + VEC + c.xl, R[ic][yy]);
     }
     // ---- r(j) on the one-point ring of the tile, spread over all warps ------------------------
-    {
+    if (NM != 2) {
         const int lane = c.tid & 31, w = c.tid >> 5;
 #pragma unroll
         for (int base = 0; base < G::NRING; base += M3_THREADS) {
@@ -166,7 +170,7 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
     }
     __syncthreads();
     if (c.tid == 0 && j - 1 + M3_ST <= c.q_last) m3_issue<T, FZ>(c, xmap, bmap, j - 1 + M3_ST, sm);
-    if (j - 1 < c.z0) return;
+    if (NM == 2 || j - 1 < c.z0) return;
 
     // ---- output plane j-1 -------------------------------------------------------------------
     const T* r1 = c.rr + rj1 * G::RS;  // r(j-1)
@@ -215,10 +219,11 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
     }
 }
 
-template <class T, int S, bool FZ>
+template <class T, int S, bool FZ, int NM>
 __global__ void __launch_bounds__(M3_THREADS, 2)
     k_sweep3d_march(Layout L, const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap bmap,
-                    const T* __restrict__ x, T* __restrict__ xo, Terms<T> M, T sA, T sM, T omega, int planes) {
+                    const T* __restrict__ x, T* __restrict__ xo, Terms<T> M, T sA, T sM, T omega, int planes,
+                    NormOut no) {
     using G = M3<T>;
     constexpr int VEC = G::VEC;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -235,6 +240,7 @@ __global__ void __launch_bounds__(M3_THREADS, 2)
     c.y0 = blockIdx.y * G::TY;
     c.z0 = blockIdx.z * planes;
     const int z_end = min(c.z0 + planes, c.n);
+    c.z_end = z_end;
     c.q0 = c.z0 - 2;
     c.q_last = z_end + 1;
     c.yl = (threadIdx.x >> 5) * 2;
@@ -270,15 +276,17 @@ __global__ void __launch_bounds__(M3_THREADS, 2)
             V16<T>::ld(c.xs + 1 * G::XS + (c.yl + yy + 2) * G::RW + VEC + c.xl, X[1][yy]);
         }
     }
+    double nacc = 0.0;
     const int K = z_end - c.q0;  // steps k = 1..K (planes j = z0-1 .. z_end)
     for (int kb = 0; kb <= K; kb += 12) {
 #define M3STEP(p)                                                                            \
     if (kb + (p) >= 1 && kb + (p) <= K)                                                     \
-        m3_step<T, S, FZ, (p)>(c, &xmap, &bmap, kb + (p), X, R, M, sA, sM, omega);
+        m3_step<T, S, FZ, NM, (p)>(c, &xmap, &bmap, kb + (p), X, R, M, sA, sM, omega, nacc);
         M3STEP(0) M3STEP(1) M3STEP(2) M3STEP(3) M3STEP(4) M3STEP(5)
         M3STEP(6) M3STEP(7) M3STEP(8) M3STEP(9) M3STEP(10) M3STEP(11)
 #undef M3STEP
     }
+    if (NM) norm_epilogue(nacc, no);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -311,13 +319,13 @@ static cudaError_t make_map(CUtensorMap* map, const Layout& L, const T* base, in
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <class T, int S, bool FZ>
+template <class T, int S, bool FZ, int NM>
 cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
-                                 T omega, cudaStream_t s) {
+                                 T omega, const NormOut& no, cudaStream_t s) {
     using G = M3<T>;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_sweep3d_march<T, S, FZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k_sweep3d_march<T, S, FZ, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)G::smem);
         if (e != cudaSuccess) return e;
         attr = true;
@@ -331,7 +339,7 @@ cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo,
     if (e != cudaSuccess) return e;
     static int occ = 0;
     if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep3d_march<T, S, FZ>, M3_THREADS, G::smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep3d_march<T, S, FZ, NM>, M3_THREADS, G::smem);
         if (occ <= 0) occ = 1;
     }
     const int tx = (L.n + G::TX - 1) / G::TX, ty = (L.n + G::TY - 1) / G::TY;
@@ -341,20 +349,22 @@ cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo,
     if (planes < 8) planes = 8;
     chunks = (L.n + planes - 1) / planes;
     dim3 g(tx, ty, chunks);
-    k_sweep3d_march<T, S, FZ><<<g, M3_THREADS, G::smem, s>>>(L, xm, bm, x, xo, M, sA, sM, omega, planes);
+    k_sweep3d_march<T, S, FZ, NM><<<g, M3_THREADS, G::smem, s>>>(L, xm, bm, x, xo, M, sA, sM, omega, planes, no);
     return cudaGetLastError();
 }
 
-#define SPAIMG_M3_INST(T, S)                                                                                       \
-    template cudaError_t launch_sweep3d_march<T, S, false>(const Layout&, const T*, const T*, T*, const Terms<T>&, \
-                                                           T, T, T, cudaStream_t);                               \
-    template cudaError_t launch_sweep3d_march<T, S, true>(const Layout&, const T*, const T*, T*, const Terms<T>&,  \
-                                                          T, T, T, cudaStream_t);
-SPAIMG_M3_INST(double, SHAPE_GENERIC)
-SPAIMG_M3_INST(double, SHAPE_C1)
-SPAIMG_M3_INST(double, SHAPE_STAR7)
-SPAIMG_M3_INST(float, SHAPE_GENERIC)
-SPAIMG_M3_INST(float, SHAPE_C1)
-SPAIMG_M3_INST(float, SHAPE_STAR7)
+#define SPAIMG_M3_INST(T, S, FZ, NM)                                                                           \
+    template cudaError_t launch_sweep3d_march<T, S, FZ, NM>(const Layout&, const T*, const T*, T*, const Terms<T>&, \
+                                                            T, T, T, const NormOut&, cudaStream_t);
+#define SPAIMG_M3_INST4(T, S) \
+    SPAIMG_M3_INST(T, S, false, 0) SPAIMG_M3_INST(T, S, true, 0) SPAIMG_M3_INST(T, S, false, 1) SPAIMG_M3_INST(T, S, true, 1)
+SPAIMG_M3_INST4(double, SHAPE_GENERIC)
+SPAIMG_M3_INST4(double, SHAPE_C1)
+SPAIMG_M3_INST4(double, SHAPE_STAR7)
+SPAIMG_M3_INST4(float, SHAPE_GENERIC)
+SPAIMG_M3_INST4(float, SHAPE_C1)
+SPAIMG_M3_INST4(float, SHAPE_STAR7)
+SPAIMG_M3_INST(double, SHAPE_C1, false, 2)
+SPAIMG_M3_INST(float, SHAPE_C1, false, 2)
 
 }  // namespace spaimg

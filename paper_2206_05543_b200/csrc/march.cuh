@@ -78,3 +78,49 @@ inline int num_sms() {
 }
 
 }  // namespace spaimg
+
+namespace spaimg {
+
+// Deterministic residual-norm epilogue shared by the fused kernels: each CTA reduces its
+// threads' partial sums of r^2 (fixed shuffle tree, fixed warp order), stores the CTA partial,
+// and the last CTA to finish (atomic ticket) adds all partials in index order and appends
+// sqrt(sum) to the device-side residual history at *slot (then advances *slot).  The result is
+// independent of CTA scheduling; no floating-point atomics.
+
+
+__device__ __forceinline__ void norm_epilogue(double s, const NormOut& no) {
+    __shared__ double red[32];
+    __shared__ bool last;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int nw = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if (l == 0) red[w] = s;
+    __syncthreads();
+    const unsigned nblocks = gridDim.x * gridDim.y * gridDim.z;
+    const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < nw; ++i) t += red[i];
+        no.partials[bid] = t;
+        __threadfence();
+        last = atomicAdd(no.counter, 1u) == nblocks - 1;
+    }
+    __syncthreads();
+    if (last && w == 0) {
+        __threadfence();
+        double t = 0.0;
+        for (unsigned i = l; i < nblocks; i += 32) t += ((volatile double*)no.partials)[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (l == 0) {
+            const int sl = *no.slot;
+            no.norms[sl] = sqrt(t);
+            *no.slot = sl + 1;
+            *no.counter = 0u;
+        }
+    }
+}
+
+}  // namespace spaimg

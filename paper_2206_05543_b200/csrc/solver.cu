@@ -309,7 +309,7 @@ static int prolong_t(int dim, int Nc, const void* coarse, const void* base, void
         if (int rc = load_dense<T>(sc, f.L, base, f.x[0], s)) return rc;
     // prolong(e) alone stores the interpolant (multigrid.py:125-129); with a base grid it is
     // the correction u + prolong(e) of multigrid.py:184.
-    CK(launch_prolong_correct<T>(f.L, c.L, f.x[0], c.x[0], s, base != nullptr));
+    CK(launch_prolong_correct<T>(f.L, c.L, f.x[0], f.x[0], c.x[0], s, base != nullptr));
     return store_dense<T>(sc, f.L, f.x[0], fine, s);
 }
 
@@ -388,6 +388,36 @@ struct spaimg_solver {
     virtual void stats(spaimg_solver_stats* st) const = 0;
 };
 
+// ------------------------------------------------------------------------------------------
+// device-side solve loop (reference multigrid.py:206-217) as a CUDA graph with conditional
+// nodes:   reset -> WHILE(cont) { A: norm of u_k (fused into cycle k+1's first pre-sweep);
+//                                 check: cont = !(k>=1 && ||r_k|| <= tol ||r_0||) && k < max;
+//                                 IF(cont) { B: rest of cycle k+1 } }
+// No host round trip per cycle; the history stays on the device until the loop ends.
+// ------------------------------------------------------------------------------------------
+struct SolveCtl {
+    double tol;
+    int max_iters;
+    int pad;
+};
+
+__global__ void k_solve_reset(int* slot, int* state) {
+    *slot = 0;
+    state[0] = 0;
+    state[1] = 0;
+}
+
+__global__ void k_solve_check(const double* norms, const int* slot, const SolveCtl* ctl, int* state,
+                              cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hi) {
+    const int k = *slot - 1;  // norms[0..k] are known: k cycles done
+    const bool conv = k >= 1 && norms[k] <= ctl->tol * norms[0];
+    const bool cont = !conv && k < ctl->max_iters;
+    state[0] = k;
+    state[1] = conv ? 1 : 0;
+    cudaGraphSetConditional(hw, cont ? 1u : 0u);
+    cudaGraphSetConditional(hi, cont ? 1u : 0u);
+}
+
 template <class T> struct Solver final : spaimg_solver {
     spaimg_mg_config cfg{};
     std::vector<double> lu_h;
@@ -395,7 +425,9 @@ template <class T> struct Solver final : spaimg_solver {
     std::vector<Level<T>> lv;  // lv[0] finest ... lv.back() = coarse-solve level
     Terms<T> M{};
     int shape = SHAPE_GENERIC;
-    bool fused = false;
+    bool fused = false;      // fused K1 sweep available for this smoother
+    bool fused_norm = false; // norm folded into the first pre-sweep (A) of the next cycle
+    bool k3_flip = false;    // (nu1+nu2) odd: the finest K3 writes the other buffer so a cycle ends in x[0]
     T omega{};
     T* lu = nullptr;
     int* piv = nullptr;
@@ -403,19 +435,24 @@ template <class T> struct Solver final : spaimg_solver {
     double* norms_d = nullptr;
     int norms_cap = 0;
     int* slot_d = nullptr;
+    int* state_d = nullptr;
+    SolveCtl* ctl_d = nullptr;
     double* partials = nullptr;
     unsigned* counter = nullptr;
     double* norms_h = nullptr;  // pinned
+    int* state_h = nullptr;     // pinned
+    SolveCtl* ctl_h = nullptr;  // pinned
     T* stage = nullptr;         // dense staging on device
-    int cur = 0;                // buffer of lv[0] holding the iterate
-    cudaGraphExec_t exec[2] = {nullptr, nullptr};
+    cudaGraphExec_t exec_cycle = nullptr, exec_solve = nullptr;
     int kernels_per_cycle = 0;
+    int kernels_a = 0;
     bool use_graph = true;
     std::vector<void*> owned;
+    std::vector<std::pair<long long, cudaGraphExec_t>> op_graphs;
 
     ~Solver() override {
-        for (int i = 0; i < 2; ++i)
-            if (exec[i]) cudaGraphExecDestroy(exec[i]);
+        if (exec_cycle) cudaGraphExecDestroy(exec_cycle);
+        if (exec_solve) cudaGraphExecDestroy(exec_solve);
         for (auto& kv : op_graphs) cudaGraphExecDestroy(kv.second);
         for (void* p : owned) cudaFree(p);
         if (norms_h) cudaFreeHost(norms_h);
@@ -423,12 +460,15 @@ template <class T> struct Solver final : spaimg_solver {
 
     template <class U> int dalloc(U** p, size_t count) {
         void* q = nullptr;
-        CK(cudaMalloc(&q, count * sizeof(U) > 0 ? count * sizeof(U) : 16));
+        const size_t bytes = count * sizeof(U) > 0 ? count * sizeof(U) : 16;
+        CK(cudaMalloc(&q, bytes));
         owned.push_back(q);
-        CK(cudaMemset(q, 0, count * sizeof(U)));
+        CK(cudaMemset(q, 0, bytes));
         *p = static_cast<U*>(q);
         return 0;
     }
+
+    NormOut norm_sink() const { return NormOut{partials, counter, norms_d, slot_d}; }
 
     int init(const spaimg_mg_config& c) {
         cfg = c;
@@ -442,6 +482,7 @@ template <class T> struct Solver final : spaimg_solver {
         shape = detect_shape(c.M);
         fused = stencil_radius(c.M) <= 1 && sweep_fused_supported(c.dim, shape);
         omega = (T)c.omega;
+        k3_flip = ((c.nu1 + c.nu2) & 1) != 0;
         // levels: halve until N <= coarsest_N (multigrid.py:166, :178)
         int N = c.N;
         while (true) {
@@ -454,7 +495,8 @@ template <class T> struct Solver final : spaimg_solver {
             if (int rc = dalloc(&l.b, (size_t)l.L.alloc)) return rc;
             if (!coarse) {
                 if (int rc = dalloc(&l.x[1], (size_t)l.L.alloc)) return rc;
-                if (int rc = dalloc(&l.r, (size_t)l.L.alloc)) return rc;
+                if (!fused || c.dim == 3 || getenv("SPAIMG_RESTRICT_V1"))  // scratch r (unfused paths)
+                    if (int rc = dalloc(&l.r, (size_t)l.L.alloc)) return rc;
             }
             lv.push_back(l);
             if (coarse) break;
@@ -464,6 +506,7 @@ template <class T> struct Solver final : spaimg_solver {
         }
         if (N != c.coarse_N || count_of(c.dim, N) != c.coarse_n)
             return fail(SPAIMG_EINVAL, "coarse factorisation does not match the coarsest level");
+        fused_norm = nsmooth() >= 1 && c.nu1 >= 1 && fused && sweep_norm_supported();
         nlu = c.coarse_n;
         std::vector<T> luT(lu_h.begin(), lu_h.end());
         if (int rc = dalloc(&lu, luT.size())) return rc;
@@ -473,18 +516,37 @@ template <class T> struct Solver final : spaimg_solver {
         norms_cap = 4097;
         if (int rc = dalloc(&norms_d, norms_cap)) return rc;
         if (int rc = dalloc(&slot_d, 1)) return rc;
-        if (int rc = dalloc(&partials, kNormBlocks)) return rc;
+        if (int rc = dalloc(&state_d, 2)) return rc;
+        if (int rc = dalloc(&ctl_d, 1)) return rc;
+        if (int rc = dalloc(&partials, 1 << 16)) return rc;
         if (int rc = dalloc(&counter, 1)) return rc;
         if (int rc = dalloc(&stage, (size_t)count_of(c.dim, c.N))) return rc;
-        CK(cudaMallocHost(&norms_h, sizeof(double) * norms_cap));
+        // one pinned block: norms | state | ctl
+        void* ph = nullptr;
+        CK(cudaMallocHost(&ph, sizeof(double) * norms_cap + 64 + sizeof(SolveCtl)));
+        norms_h = static_cast<double*>(ph);
+        state_h = reinterpret_cast<int*>(norms_h + norms_cap);
+        ctl_h = reinterpret_cast<SolveCtl*>(reinterpret_cast<char*>(state_h) + 64);
         return 0;
     }
 
     int nsmooth() const { return (int)lv.size() - 1; }
 
+    // ||b - A x||_2 of the finest level appended to the device history
+    int norm_launch(const T* x, cudaStream_t s, int* launches) {
+        const Level<T>& L = lv[0];
+        if (sweep_norm_supported()) {
+            CK(launch_norm_march<T>(L.L, x, L.b, L.sA, norm_sink(), s));
+        } else {
+            CK(launch_residual_norm<T>(L.L, x, L.b, L.sA, partials, counter, norms_d, 0, slot_d, s));
+        }
+        ++*launches;
+        return 0;
+    }
+
     // recursive schedule (multigrid.py:157-185).  Returns the buffer index of level l holding
-    // the result, or -1 on error.
-    int visit(int l, int a, bool fz, cudaStream_t s, int* launches) {
+    // the result, or -1 on error.  pre_done: the first pre-sweep of level 0 already ran (A).
+    int visit(int l, int a, bool fz, cudaStream_t s, int* launches, bool pre_done) {
         Level<T>& L = lv[l];
         if (l == nsmooth()) {  // u.N <= coarsest_N: direct solve (multigrid.py:166-167)
             if (launch_coarse_solve<T>(L.L, L.b, L.x[0], lu, piv, nlu, s) != cudaSuccess) return -1;
@@ -492,7 +554,8 @@ template <class T> struct Solver final : spaimg_solver {
             return 0;
         }
         for (int k = 0; k < cfg.nu1; ++k) {
-            if (do_sweep<T>(L, a, fz, M, shape, fused, omega, s, launches)) return -1;
+            if (!(l == 0 && pre_done && k == 0))
+                if (do_sweep<T>(L, a, fz, M, shape, fused, omega, s, launches)) return -1;
             a = 1 - a;
             fz = false;
         }
@@ -509,12 +572,14 @@ template <class T> struct Solver final : spaimg_solver {
             ++*launches;
             c = 0;
         } else {
-            c = visit(l + 1, 0, true, s, launches);
-            for (int g = 1; g < cfg.gamma && c >= 0; ++g) c = visit(l + 1, c, false, s, launches);
+            c = visit(l + 1, 0, true, s, launches, false);
+            for (int g = 1; g < cfg.gamma && c >= 0; ++g) c = visit(l + 1, c, false, s, launches, false);
             if (c < 0) return -1;
         }
-        if (launch_prolong_correct<T>(L.L, C.L, L.x[a], C.x[c], s) != cudaSuccess) return -1;
+        const int ao = (l == 0 && k3_flip) ? 1 - a : a;
+        if (launch_prolong_correct<T>(L.L, C.L, L.x[a], L.x[ao], C.x[c], s) != cudaSuccess) return -1;
         ++*launches;
+        a = ao;
         for (int k = 0; k < cfg.nu2; ++k) {
             if (do_sweep<T>(L, a, false, M, shape, fused, omega, s, launches)) return -1;
             a = 1 - a;
@@ -522,67 +587,117 @@ template <class T> struct Solver final : spaimg_solver {
         return a;
     }
 
-    int norm_into_history(int a, cudaStream_t s) {
-        CK(launch_residual_norm<T>(lv[0].L, lv[0].x[a], lv[0].b, lv[0].sA, partials, counter, norms_d, 0, slot_d, s));
+    // A: norm of the iterate in x[0] (+ the first pre-sweep of the next cycle when fused)
+    int part_a(cudaStream_t s, int* launches) {
+        if (fused_norm) {
+            Level<T>& L = lv[0];
+            const NormOut no = norm_sink();
+            CK(launch_sweep<T>(L.L, L.x[0], L.b, L.x[1], M, shape, L.sA, L.sM, omega, false, s, &no));
+            ++*launches;
+            return 0;
+        }
+        return norm_launch(lv[0].x[0], s, launches);
+    }
+
+    // B: the rest of the cycle; ends with the iterate back in x[0]
+    int part_b(cudaStream_t s, int* launches) {
+        const int out = visit(0, 0, false, s, launches, fused_norm);
+        if (out != 0) return fail(SPAIMG_EINVAL, out < 0 ? "cycle launch failed: " + g_err : "cycle parity error");
         return 0;
     }
 
-    // one cycle + its residual norm, starting from lv[0].x[a]; returns the final buffer
-    int cycle_body(int a, cudaStream_t s, int* launches) {
-        const int out = visit(0, a, false, s, launches);
-        if (out < 0) return -1;
-        if (nsmooth() == 0) {
-            // single-level problem: the cycle IS the direct solve into x[0]
-        }
-        if (norm_into_history(out, s)) return -1;
-        ++*launches;
-        return out;
-    }
-
-    int build_graph(int a) {
+    template <class F> int capture_into(cudaGraph_t g, F&& body) {
         cudaStream_t cs;
         CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-        cudaGraph_t g;
-        cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+        cudaError_t e = cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
         if (e != cudaSuccess) {
             cudaStreamDestroy(cs);
             return fail((int)e, std::string("begin capture: ") + cudaGetErrorString(e));
         }
-        int launches = 0;
-        const int out = cycle_body(a, cs, &launches);
-        e = cudaStreamEndCapture(cs, &g);
+        const int rc = body(cs);
+        cudaGraph_t out;
+        e = cudaStreamEndCapture(cs, &out);
         cudaStreamDestroy(cs);
-        if (out < 0) {
-            if (e == cudaSuccess) cudaGraphDestroy(g);
-            return fail(SPAIMG_EINVAL, "cycle capture failed: " + g_err);
-        }
+        if (rc) return rc;
         if (e != cudaSuccess) return fail((int)e, std::string("end capture: ") + cudaGetErrorString(e));
-        e = cudaGraphInstantiate(&exec[a], g, 0);
-        cudaGraphDestroy(g);
-        if (e != cudaSuccess) return fail((int)e, std::string("graph instantiate: ") + cudaGetErrorString(e));
-        kernels_per_cycle = launches;
         return 0;
     }
 
-    int final_buffer(int a) const {
-        if (nsmooth() == 0) return 0;
-        return (cfg.nu1 + cfg.nu2) % 2 ? 1 - a : a;
+    // add a conditional node after the current capture dependencies of cs; returns its body
+    int add_conditional(cudaStream_t cs, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type,
+                        cudaGraph_t* body) {
+        cudaStreamCaptureStatus st;
+        cudaGraph_t cg;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        CK(cudaStreamGetCaptureInfo(cs, &st, nullptr, &cg, &deps, &nd));
+        cudaGraphNodeParams p{};
+        p.type = cudaGraphNodeTypeConditional;
+        p.conditional.handle = h;
+        p.conditional.type = type;
+        p.conditional.size = 1;
+        cudaGraphNode_t node;
+        CK(cudaGraphAddNode(&node, cg, deps, nd, &p));
+        CK(cudaStreamUpdateCaptureDependencies(cs, &node, 1, cudaStreamSetCaptureDependencies));
+        *body = p.conditional.phGraph_out[0];
+        return 0;
     }
 
-    int one_cycle(cudaStream_t s) {
-        if (use_graph) {
-            if (!exec[cur])
-                if (int rc = build_graph(cur)) return rc;
-            CK(cudaGraphLaunch(exec[cur], s));
-            cur = final_buffer(cur);
-            return 0;
+    int build_solve_graph() {
+        cudaGraph_t g;
+        CK(cudaGraphCreate(&g, 0));
+        int launches_a = 0, launches_b = 0;
+        cudaGraphConditionalHandle hw, hi;
+        cudaGraph_t wbody = nullptr, ibody = nullptr;
+        int rc = 0;
+        cudaError_t e = cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault);
+        if (e != cudaSuccess) rc = fail((int)e, "conditional handle");
+        if (!rc)
+            rc = capture_into(g, [&](cudaStream_t cs) -> int {
+                k_solve_reset<<<1, 1, 0, cs>>>(slot_d, state_d);
+                CK(cudaGetLastError());
+                return add_conditional(cs, hw, cudaGraphCondTypeWhile, &wbody);
+            });
+        if (!rc) {
+            e = cudaGraphConditionalHandleCreate(&hi, wbody, 0, cudaGraphCondAssignDefault);
+            if (e != cudaSuccess) rc = fail((int)e, "conditional handle (if)");
         }
+        if (!rc)
+            rc = capture_into(wbody, [&](cudaStream_t cs) -> int {
+                if (int r = part_a(cs, &launches_a)) return r;
+                k_solve_check<<<1, 1, 0, cs>>>(norms_d, slot_d, ctl_d, state_d, hw, hi);
+                CK(cudaGetLastError());
+                ++launches_a;
+                return add_conditional(cs, hi, cudaGraphCondTypeIf, &ibody);
+            });
+        if (!rc) rc = capture_into(ibody, [&](cudaStream_t cs) -> int { return part_b(cs, &launches_b); });
+        if (!rc) {
+            e = cudaGraphInstantiate(&exec_solve, g, 0);
+            if (e != cudaSuccess) rc = fail((int)e, std::string("solve graph instantiate: ") + cudaGetErrorString(e));
+        }
+        cudaGraphDestroy(g);
+        if (!rc) {
+            kernels_per_cycle = launches_a + launches_b;
+            kernels_a = launches_a;
+        }
+        return rc;
+    }
+
+    int build_cycle_graph() {
+        cudaGraph_t g;
+        CK(cudaGraphCreate(&g, 0));
         int launches = 0;
-        const int out = cycle_body(cur, s, &launches);
-        if (out < 0) return fail(SPAIMG_EINVAL, "cycle failed: " + g_err);
-        kernels_per_cycle = launches;
-        cur = out;
-        return 0;
+        int rc = capture_into(g, [&](cudaStream_t cs) -> int {
+            const int out = visit(0, 0, false, cs, &launches, false);
+            if (out != 0) return fail(SPAIMG_EINVAL, "cycle capture failed: " + g_err);
+            return norm_launch(lv[0].x[0], cs, &launches);
+        });
+        if (!rc) {
+            cudaError_t e = cudaGraphInstantiate(&exec_cycle, g, 0);
+            if (e != cudaSuccess) rc = fail((int)e, "cycle graph instantiate");
+        }
+        cudaGraphDestroy(g);
+        return rc;
     }
 
     int load(const void* b, const void* u0, cudaStream_t s) override {
@@ -590,7 +705,6 @@ template <class T> struct Solver final : spaimg_solver {
         Level<T>& L = lv[0];
         if (b)  // NULL keeps the right-hand side already loaded
             if (int rc = load_dense<T>(sc, L.L, b, L.b, s, stage)) return rc;
-        cur = 0;
         if (u0) {
             if (int rc = load_dense<T>(sc, L.L, u0, L.x[0], s, stage)) return rc;
         } else {
@@ -600,31 +714,58 @@ template <class T> struct Solver final : spaimg_solver {
         return 0;
     }
 
+    // n full cycles (each appends its residual norm to the device history)
     int cycles(int n, cudaStream_t s) override {
-        for (int k = 0; k < n; ++k)
-            if (int rc = one_cycle(s)) return rc;
+        if (use_graph && !exec_cycle)
+            if (int rc = build_cycle_graph()) return rc;
+        for (int k = 0; k < n; ++k) {
+            if (use_graph) {
+                CK(cudaGraphLaunch(exec_cycle, s));
+            } else {
+                int launches = 0;
+                if (visit(0, 0, false, s, &launches, false) != 0) return fail(SPAIMG_EINVAL, "cycle failed: " + g_err);
+                if (int rc = norm_launch(lv[0].x[0], s, &launches)) return rc;
+            }
+        }
         return 0;
     }
 
     int run(double tol, int max_iters, double* norms, int* iters, int* conv, cudaStream_t s) override {
         if (max_iters + 1 > norms_cap) return fail(SPAIMG_EINVAL, "max_iters too large");
-        CK(cudaMemsetAsync(slot_d, 0, sizeof(int), s));
-        if (int rc = norm_into_history(cur, s)) return rc;
-        CK(cudaMemcpyAsync(norms_h, norms_d, sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (!use_graph) return run_host_loop(tol, max_iters, norms, iters, conv, s);
+        if (!exec_solve)
+            if (int rc = build_solve_graph()) return rc;
+        ctl_h->tol = tol;
+        ctl_h->max_iters = max_iters;
+        CK(cudaMemcpyAsync(ctl_d, ctl_h, sizeof(SolveCtl), cudaMemcpyHostToDevice, s));
+        CK(cudaGraphLaunch(exec_solve, s));
+        CK(cudaMemcpyAsync(state_h, state_d, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(norms_h, norms_d, sizeof(double) * (max_iters + 1), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        norms[0] = norms_h[0];
-        int k = 0;
+        const int k = state_h[0];
+        for (int i = 0; i <= k; ++i) norms[i] = norms_h[i];
+        *iters = k;
+        *conv = state_h[1];
+        return 0;
+    }
+
+    // eager variant (SPAIMG_NO_GRAPH=1): same schedule, one host round trip per cycle
+    int run_host_loop(double tol, int max_iters, double* norms, int* iters, int* conv, cudaStream_t s) {
+        CK(cudaMemsetAsync(slot_d, 0, sizeof(int), s));
+        int launches = 0, k = 0;
         *conv = 0;
-        while (k < max_iters) {
-            if (int rc = one_cycle(s)) return rc;
-            ++k;
+        while (true) {
+            if (int rc = part_a(s, &launches)) return rc;
             CK(cudaMemcpyAsync(norms_h + k, norms_d + k, sizeof(double), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             norms[k] = norms_h[k];
-            if (norms[k] <= tol * norms[0]) {
+            if (k >= 1 && norms[k] <= tol * norms[0]) {
                 *conv = 1;
                 break;
             }
+            if (k >= max_iters) break;
+            if (int rc = part_b(s, &launches)) return rc;
+            ++k;
         }
         *iters = k;
         return 0;
@@ -632,48 +773,54 @@ template <class T> struct Solver final : spaimg_solver {
 
     int store(void* out, cudaStream_t s) override {
         Scratch sc(s);
-        return store_dense<T>(sc, lv[0].L, lv[0].x[cur], out, s, stage);
+        return store_dense<T>(sc, lv[0].L, lv[0].x[0], out, s, stage);
     }
 
     int op_launch(int which, cudaStream_t s) {
         Level<T>& L = lv[0];
         if (nsmooth() < 1) return fail(SPAIMG_EINVAL, "no smoothing level");
+        int launches = 0;
         switch (which) {
-            case 0: return do_sweep<T>(L, cur, false, M, shape, fused, omega, s, nullptr);
-            case 1: CK(launch_residual_restrict<T>(L.L, lv[1].L, L.x[cur], L.b, lv[1].b, L.sA, L.r, s)); return 0;
-            case 2: CK(launch_prolong_correct<T>(L.L, lv[1].L, L.x[1 - cur], lv[1].x[0], s)); return 0;
-            case 3:
-                CK(launch_residual_norm<T>(L.L, L.x[cur], L.b, L.sA, partials, counter, norms_d, 0, nullptr, s));
-                return 0;
+            case 0: return do_sweep<T>(L, 0, false, M, shape, fused, omega, s, nullptr);
+            case 1: CK(launch_residual_restrict<T>(L.L, lv[1].L, L.x[0], L.b, lv[1].b, L.sA, L.r, s)); return 0;
+            case 2: CK(launch_prolong_correct<T>(L.L, lv[1].L, L.x[1], L.x[1], lv[1].x[0], s)); return 0;
+            case 3: {
+                // keep the history cursor in range while timing repeated norms
+                CK(cudaMemsetAsync(slot_d, 0, sizeof(int), s));
+                return norm_launch(L.x[0], s, &launches);
+            }
+            case 4: {  // fused sweep + norm (part A)
+                CK(cudaMemsetAsync(slot_d, 0, sizeof(int), s));
+                return part_a(s, &launches);
+            }
             default: return fail(SPAIMG_EINVAL, "unknown op");
         }
     }
 
     // `reps` back-to-back launches of one kernel, replayed from a cached CUDA graph so the
     // per-launch time excludes host launch gaps (used for per-operator timing)
-    std::vector<std::pair<long long, cudaGraphExec_t>> op_graphs;
     int op(int which, int reps, cudaStream_t s) override {
         if (reps <= 1) return reps == 1 ? op_launch(which, s) : 0;
-        const long long key = ((long long)which * 1000003 + reps) * 2 + cur;
+        const long long key = (long long)which * 1000003 + reps;
         for (auto& kv : op_graphs)
             if (kv.first == key) {
                 CK(cudaGraphLaunch(kv.second, s));
                 return 0;
             }
-        cudaStream_t cs;
-        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
         cudaGraph_t g;
-        CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-        int rc = 0;
-        for (int k = 0; k < reps && !rc; ++k) rc = op_launch(which, cs);
-        cudaError_t e = cudaStreamEndCapture(cs, &g);
-        cudaStreamDestroy(cs);
-        if (rc) return rc;
-        if (e != cudaSuccess) return fail((int)e, "op capture failed");
-        cudaGraphExec_t ex;
-        e = cudaGraphInstantiate(&ex, g, 0);
+        CK(cudaGraphCreate(&g, 0));
+        int rc = capture_into(g, [&](cudaStream_t cs) -> int {
+            for (int k = 0; k < reps; ++k)
+                if (int r = op_launch(which, cs)) return r;
+            return 0;
+        });
+        cudaGraphExec_t ex = nullptr;
+        if (!rc) {
+            cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
+            if (e != cudaSuccess) rc = fail((int)e, "op graph instantiate failed");
+        }
         cudaGraphDestroy(g);
-        if (e != cudaSuccess) return fail((int)e, "op graph instantiate failed");
+        if (rc) return rc;
         op_graphs.push_back({key, ex});
         CK(cudaGraphLaunch(ex, s));
         return 0;
@@ -682,6 +829,7 @@ template <class T> struct Solver final : spaimg_solver {
     void stats(spaimg_solver_stats* st) const override {
         st->levels = nsmooth();
         st->kernels_per_cycle = kernels_per_cycle;
+        st->kernels_stop_test = kernels_a;
         st->unknowns = count_of(cfg.dim, cfg.N);
         st->graph = use_graph ? 1 : 0;
         st->fused_sweep = fused ? 1 : 0;

@@ -105,6 +105,14 @@ template <> struct ShapeT<SHAPE_STAR7> {
     }
 };
 
+// Device-side residual-history sink of the fused norm (see march.cuh norm_epilogue).
+struct NormOut {
+    double* partials;   // >= number of CTAs
+    unsigned* counter;  // zero on entry, re-armed to zero by the last CTA
+    double* norms;      // residual history
+    int* slot;          // history cursor
+};
+
 // ------------------------------------------------------------------------------------------
 // per-point expression trees
 // ------------------------------------------------------------------------------------------
