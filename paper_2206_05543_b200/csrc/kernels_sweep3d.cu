@@ -185,9 +185,18 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
             T acc = T(0);
+            if constexpr (S == SHAPE_GENERIC) {
+                // runtime term list: every r value (own points included) is in the shared r ring,
+                // so a rolled loop keeps the 12-step unrolled body small
+#pragma unroll 1
+                for (int t = 0; t < nt; ++t) {
+                    const int o0 = M.off[t][0];
+                    const T* pl = o0 == 0 ? r1 : (o0 > 0 ? r0 : r2);
+                    acc = O::add(acc, O::mul(M.c[t], pl[so + M.off[t][1] * RW + v + M.off[t][2]]));
+                }
+            } else {
 #pragma unroll
-            for (int t = 0; t < (S == SHAPE_GENERIC ? kMaxTerms : ShapeT<(S == SHAPE_GENERIC ? 1 : S)>::nt); ++t) {
-                if (S == SHAPE_GENERIC && t >= nt) break;
+            for (int t = 0; t < ShapeT<(S == SHAPE_GENERIC ? 1 : S)>::nt; ++t) {
                 const int o0 = toff<T, S>(M, t, 0), o1 = toff<T, S>(M, t, 1), o2 = toff<T, S>(M, t, 2);
                 T val;
                 if (o1 == 0 && o2 == 0) {
@@ -201,6 +210,7 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
                     val = pl[so + o1 * RW + v + o2];
                 }
                 acc = O::add(acc, O::mul(M.c[t], val));
+            }
             }
             out[v] = relax<T>(FZ ? T(0) : X[im][yy][v], acc, sM, omega);
         }

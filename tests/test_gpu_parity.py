@@ -194,3 +194,35 @@ def test_full_size_properties_2d():
     u2, r2 = sp.solve(sp.Grid(N, dev(b)), cfg, u0=0)
     assert r1.residual_norms == r2.residual_norms
     assert torch.equal(u1.values, u2.values)
+
+
+def _custom_stencils(dim):
+    """Radius-1 stencils that hit the generic (runtime term list) kernels: a reversed-order
+    copy of the paper's smoother and a full box with distinct coefficients."""
+    from fractions import Fraction
+    base = sp.named("m9" if dim == 2 else "m7").stencil
+    rev = sp.Stencil(dim, dict(reversed(list(base.entries.items()))), base.h_exponent)
+    import itertools
+    box = {}
+    for k, o in enumerate(itertools.product((0, 1, -1), repeat=dim)):
+        box[o] = Fraction(1, 7 + k) if any(o) else Fraction(3, 4)
+    return {"reversed": (rev, 0.15), "box": (sp.Stencil(dim, box, 2), 0.05)}
+
+
+@pytest.mark.parametrize("dim,N", [(2, 66), (3, 34)])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_generic_stencils_vs_oracle(dim, N, dtype):
+    rng = np.random.default_rng(7 * N + dim)
+    x = rng.uniform(-1, 1, (N - 1,) * dim)
+    b = rng.uniform(-1, 1, (N - 1,) * dim)
+    npdt = np.float64 if dtype == "float64" else np.float32
+    tdt = torch.float64 if dtype == "float64" else torch.float32
+    u, bb = sp.Grid(N, dev(x, tdt)), sp.Grid(N, dev(b, tdt))
+    for name, (M, om) in _custom_stencils(dim).items():
+        mt = npo.terms_of(M)
+        got = host(sp.smooth(u, bb, M, om, 3))
+        assert np.array_equal(got, c_oracle.smooth(x, b, N, mt, om, 3, dtype=npdt)), name
+        if dtype == "float64":
+            cfg = sp.MgConfig(smoother=M, omega=om, cycle="V", nu1=1, nu2=1, coarsest_N=2)
+            got = host(sp.cycle(u, bb, cfg))
+            assert np.array_equal(got, c_oracle.cycle(x, b, N, mt, om, 1, 1, 1, 2)), name
