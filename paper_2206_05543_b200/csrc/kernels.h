@@ -58,4 +58,33 @@ template <class T>
 cudaError_t launch_coarse_solve(const Layout& L, const T* b, T* x, const T* lu, const int* piv, int nlu,
                                 cudaStream_t s);
 
+// K5+: single-block tail of the cycle (kernels_tail.cu): every level from a threshold down
+// runs inside one CTA, interpreting the host-recorded op list of the recursion.
+enum TailOpType { TAIL_SWEEP = 0, TAIL_ZERO = 1, TAIL_RESTRICT = 2, TAIL_PROLONG = 3, TAIL_COARSE = 4 };
+struct TailOp {
+    int type;
+    int level;  // index into TailArgs::lv
+    int a_in, a_out;  // x buffer indices of the level
+    int c;            // PROLONG: x buffer of the coarse level holding the correction
+    int fz;           // SWEEP: the input iterate is zero (x not read)
+};
+template <class T> struct TailLevel {
+    Layout L;
+    T* x[2];
+    T* b;
+    T* r;
+    T sA, sM;
+};
+template <class T> struct TailArgs {
+    const TailLevel<T>* lv;  // device array
+    const TailOp* ops;       // device array
+    int nops;
+    Terms<T> M;
+    T omega;
+    const T* lu;
+    const int* piv;
+    int nlu;
+};
+template <class T> cudaError_t launch_tail(const TailArgs<T>& a, cudaStream_t s);
+
 }  // namespace spaimg

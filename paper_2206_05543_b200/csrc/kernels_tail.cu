@@ -1,0 +1,231 @@
+// K5+: single-block coarse-level path.  All levels at or below a size threshold -- every
+// smoothing sweep, residual + restriction, the coarse direct solve and every prolongation +
+// correction of the tail of the V/W recursion (reference multigrid.py:157-185) -- run inside
+// ONE CTA of 1024 threads, phase after phase separated by __syncthreads(), instead of one
+// graph node per operation.  The host walks the same recursion as the multi-kernel schedule
+// and records it as a list of TailOps; the kernel interprets that list.
+//
+// Data stays in the levels' own padded buffers (global memory, L1/L2 resident at these
+// sizes: 2D N<=64 is <= 32 KB of interior per vector).  All loads are plain (coherent) loads:
+// after __syncthreads() every write of the block is visible to the block, which is the only
+// ordering the schedule needs.  Every per-point expression is the same Appendix-A tree as the
+// multi-kernel path (spaimg_common.cuh), so the tail is bitwise identical to it.
+#include "kernels.h"
+#include "march.cuh"
+
+namespace spaimg {
+
+constexpr int kTailThreads = 1024;
+
+__device__ __forceinline__ long long tidx(const Layout& L, int i0, int i1, int i2) {
+    return L.origin + (long long)i0 * (L.dim == 2 ? L.px : L.pp) + (L.dim == 2 ? (long long)i1 : (long long)i1 * L.px + i2);
+}
+
+// interior point q (C order) -> padded index
+__device__ __forceinline__ long long tpoint(const Layout& L, int q) {
+    const int n = L.n;
+    if (L.dim == 2) return L.origin + (long long)(q / n) * L.px + (q % n);
+    const int i0 = q / (n * n), rem = q - i0 * n * n;
+    return L.origin + (long long)i0 * L.pp + (long long)(rem / n) * L.px + (rem % n);
+}
+
+template <class T>
+__device__ __forceinline__ T tail_residual(const Layout& L, const T* x, const T* b, long long p, T sA) {
+    if (L.dim == 2) return residual2d<T>(b[p], x[p], x[p + L.px], x[p - L.px], x[p + 1], x[p - 1], sA);
+    return residual3d<T>(b[p], x[p], x[p + L.pp], x[p - L.pp], x[p + L.px], x[p - L.px], x[p + 1], x[p - 1], sA);
+}
+
+// r = b - A x on every interior point (r = b exactly when x == 0, i.e. fz)
+template <class T>
+__device__ void tail_residual_phase(const TailLevel<T>& v, const T* x, bool fz) {
+    const Layout& L = v.L;
+    const int cnt = L.dim == 2 ? L.n * L.n : L.n * L.n * L.n;
+    for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+        const long long p = tpoint(L, q);
+        v.r[p] = fz ? v.b[p] : tail_residual<T>(L, x, v.b, p, v.sA);
+    }
+}
+
+// xo = x + omega * ((M r) * sM)   (x == nullptr: from zero)
+template <class T>
+__device__ void tail_relax_phase(const TailLevel<T>& v, const T* x, T* xo, const Terms<T>& M, T omega) {
+    using O = Op<T>;
+    const Layout& L = v.L;
+    const int cnt = L.dim == 2 ? L.n * L.n : L.n * L.n * L.n;
+    for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+        const long long p = tpoint(L, q);
+        T acc = T(0);
+        for (int k = 0; k < M.nt; ++k) {
+            const long long o = L.dim == 2 ? (long long)M.off[k][0] * L.px + M.off[k][1]
+                                           : (long long)M.off[k][0] * L.pp + (long long)M.off[k][1] * L.px + M.off[k][2];
+            acc = O::add(acc, O::mul(M.c[k], v.r[p + o]));
+        }
+        xo[p] = relax<T>(x ? x[p] : T(0), acc, v.sM, omega);
+    }
+}
+
+// coarse right-hand side = full weighting of the fine residual (separable, axis 0 first)
+template <class T>
+__device__ void tail_restrict_phase(const TailLevel<T>& f, const TailLevel<T>& c) {
+    const Layout& Lf = f.L;
+    const Layout& Lc = c.L;
+    const int m = Lc.n;
+    const int cnt = Lf.dim == 2 ? m * m : m * m * m;
+    const T* r = f.r;
+    for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+        if (Lf.dim == 2) {
+            const int I = q / m, K = q % m;
+            T t[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const long long p = tidx(Lf, 2 * I + 1, 2 * K + a, 0);
+                t[a] = fw<T>(r[p - Lf.px], r[p], r[p + Lf.px]);
+            }
+            c.b[tidx(Lc, I, K, 0)] = fw<T>(t[0], t[1], t[2]);
+        } else {
+            const int I = q / (m * m), J = (q / m) % m, K = q % m;
+            T u[3];
+#pragma unroll
+            for (int qk = 0; qk < 3; ++qk) {
+                T t[3];
+#pragma unroll
+                for (int qj = 0; qj < 3; ++qj) {
+                    const long long p = tidx(Lf, 2 * I + 1, 2 * J + qj, 2 * K + qk);
+                    t[qj] = fw<T>(r[p - Lf.pp], r[p], r[p + Lf.pp]);
+                }
+                u[qk] = fw<T>(t[0], t[1], t[2]);
+            }
+            c.b[tidx(Lc, I, J, K)] = fw<T>(u[0], u[1], u[2]);
+        }
+    }
+}
+
+// interpolant of fine line index i from a coarse line accessor g(j) (zero frame outside):
+// odd i = 2j+1 -> g(j); even i = 2j -> pl_even(g(j-1), g(j)) with the reference end formulas
+template <class T, class G>
+__device__ __forceinline__ T tail_interp(int i, int m, G&& g) {
+    if (i & 1) return g((i - 1) >> 1);
+    const int j = i >> 1;
+    return pl_even<T>(g(j - 1), g(j), j == 0, j == m);
+}
+
+// xo = xi + P e  (separable d-linear prolongation, axis 0 first; in place allowed)
+template <class T>
+__device__ void tail_prolong_phase(const TailLevel<T>& f, const TailLevel<T>& c, const T* xi, T* xo, const T* e) {
+    using O = Op<T>;
+    const Layout& Lf = f.L;
+    const Layout& Lc = c.L;
+    const int m = Lc.n;
+    const int cnt = Lf.dim == 2 ? Lf.n * Lf.n : Lf.n * Lf.n * Lf.n;
+    const int n = Lf.n;
+    for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+        T val;
+        long long p;
+        if (Lf.dim == 2) {
+            const int i0 = q / n, i1 = q % n;
+            p = tidx(Lf, i0, i1, 0);
+            // axis 0 at fine row i0 for coarse column j1, then axis 1
+            auto t0 = [&](int j1) {
+                return tail_interp<T>(i0, m, [&](int j0) { return e[tidx(Lc, j0, j1, 0)]; });
+            };
+            val = tail_interp<T>(i1, m, t0);
+        } else {
+            const int i0 = q / (n * n), i1 = (q / n) % n, i2 = q % n;
+            p = tidx(Lf, i0, i1, i2);
+            auto t1 = [&](int j2) {
+                auto t0 = [&](int j1) {
+                    return tail_interp<T>(i0, m, [&](int j0) { return e[tidx(Lc, j0, j1, j2)]; });
+                };
+                return tail_interp<T>(i1, m, t0);
+            };
+            val = tail_interp<T>(i2, m, t1);
+        }
+        xo[p] = O::add(xi[p], val);
+    }
+}
+
+// getrs order (Appendix A.5/A.6), identical to k_coarse_solve
+template <class T>
+__device__ void tail_coarse_phase(const TailLevel<T>& v, T* y, const T* lu, const int* piv, int nlu) {
+    using O = Op<T>;
+    const Layout& L = v.L;
+    for (int q = threadIdx.x; q < nlu; q += blockDim.x) y[q] = v.b[tpoint(L, q)];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nlu; ++i) {
+            const int p = piv[i];
+            if (p != i) {
+                const T t = y[i];
+                y[i] = y[p];
+                y[p] = t;
+            }
+        }
+    }
+    __syncthreads();
+    for (int j = 0; j < nlu; ++j) {
+        const T yj = y[j];
+        for (int i = j + 1 + threadIdx.x; i < nlu; i += blockDim.x) y[i] = O::fma(-lu[(long long)i * nlu + j], yj, y[i]);
+        __syncthreads();
+    }
+    for (int j = nlu - 1; j >= 0; --j) {
+        if (threadIdx.x == 0) y[j] = O::div(y[j], lu[(long long)j * nlu + j]);
+        __syncthreads();
+        const T yj = y[j];
+        for (int i = threadIdx.x; i < j; i += blockDim.x) y[i] = O::fma(-lu[(long long)i * nlu + j], yj, y[i]);
+        __syncthreads();
+    }
+    for (int q = threadIdx.x; q < nlu; q += blockDim.x) v.x[0][tpoint(L, q)] = y[q];
+}
+
+template <class T>
+__global__ void __launch_bounds__(kTailThreads) k_tail(TailArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* y = reinterpret_cast<T*>(smem_raw);
+    for (int i = 0; i < a.nops; ++i) {
+        const TailOp op = a.ops[i];
+        const TailLevel<T>& v = a.lv[op.level];
+        switch (op.type) {
+            case TAIL_SWEEP:
+                tail_residual_phase<T>(v, v.x[op.a_in], op.fz);
+                __syncthreads();
+                tail_relax_phase<T>(v, op.fz ? nullptr : v.x[op.a_in], v.x[op.a_out], a.M, a.omega);
+                break;
+            case TAIL_ZERO: {
+                const Layout& L = v.L;
+                const int cnt = L.dim == 2 ? L.n * L.n : L.n * L.n * L.n;
+                for (int q = threadIdx.x; q < cnt; q += blockDim.x) v.x[op.a_out][tpoint(L, q)] = T(0);
+                break;
+            }
+            case TAIL_RESTRICT:
+                tail_residual_phase<T>(v, v.x[op.a_in], false);
+                __syncthreads();
+                tail_restrict_phase<T>(v, a.lv[op.level + 1]);
+                break;
+            case TAIL_PROLONG: {
+                const TailLevel<T>& c = a.lv[op.level + 1];
+                tail_prolong_phase<T>(v, c, v.x[op.a_in], v.x[op.a_out], c.x[op.c]);
+                break;
+            }
+            case TAIL_COARSE:
+                tail_coarse_phase<T>(v, y, a.lu, a.piv, a.nlu);
+                break;
+        }
+        __syncthreads();
+    }
+}
+
+template <class T>
+cudaError_t launch_tail(const TailArgs<T>& a, cudaStream_t s) {
+    const size_t smem = (size_t)(a.nlu > 0 ? a.nlu : 1) * sizeof(T);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_tail<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    k_tail<T><<<1, kTailThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template cudaError_t launch_tail<double>(const TailArgs<double>&, cudaStream_t);
+template cudaError_t launch_tail<float>(const TailArgs<float>&, cudaStream_t);
+
+}  // namespace spaimg

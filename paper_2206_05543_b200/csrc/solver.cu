@@ -449,6 +449,12 @@ template <class T> struct Solver final : spaimg_solver {
     bool use_graph = true;
     std::vector<void*> owned;
     std::vector<std::pair<long long, cudaGraphExec_t>> op_graphs;
+    // single-block tail: levels >= tail_l (if < nsmooth()) run in one CTA per visit
+    int tail_l = 1 << 30;
+    TailLevel<T>* tail_lv = nullptr;               // device copy of the tail levels' descriptors
+    TailOp* tail_ops[2][2] = {};  // uploaded op lists keyed by (entry buffer a, zero start)
+    int tail_nops[2][2] = {};
+    int tail_out[2][2] = {};
 
     ~Solver() override {
         if (exec_cycle) cudaGraphExecDestroy(exec_cycle);
@@ -495,7 +501,7 @@ template <class T> struct Solver final : spaimg_solver {
             if (int rc = dalloc(&l.b, (size_t)l.L.alloc)) return rc;
             if (!coarse) {
                 if (int rc = dalloc(&l.x[1], (size_t)l.L.alloc)) return rc;
-                if (!fused || c.dim == 3 || getenv("SPAIMG_RESTRICT_V1"))  // scratch r (unfused paths)
+                if (!fused || c.dim == 3 || getenv("SPAIMG_RESTRICT_V1") || N <= tail_threshold(c))  // scratch r
                     if (int rc = dalloc(&l.r, (size_t)l.L.alloc)) return rc;
             }
             lv.push_back(l);
@@ -513,6 +519,7 @@ template <class T> struct Solver final : spaimg_solver {
         CK(cudaMemcpy(lu, luT.data(), luT.size() * sizeof(T), cudaMemcpyHostToDevice));
         if (int rc = dalloc(&piv, piv_h.size())) return rc;
         CK(cudaMemcpy(piv, piv_h.data(), piv_h.size() * sizeof(int), cudaMemcpyHostToDevice));
+        if (int rc = init_tail()) return rc;
         norms_cap = 4097;
         if (int rc = dalloc(&norms_d, norms_cap)) return rc;
         if (int rc = dalloc(&slot_d, 1)) return rc;
@@ -532,6 +539,93 @@ template <class T> struct Solver final : spaimg_solver {
 
     int nsmooth() const { return (int)lv.size() - 1; }
 
+    // largest mesh count run by the single-block tail (SPAIMG_TAIL_N overrides; 0 disables)
+    static int tail_threshold(const spaimg_mg_config& c) {
+        const char* e = getenv("SPAIMG_TAIL_N");
+        if (e) return atoi(e);
+        return c.dim == 2 ? 32 : 8;  // measured optimum (tools/tune.py, c1/c2/c4)
+    }
+
+    int init_tail() {
+        const int thr = tail_threshold(cfg);
+        int l0 = nsmooth();
+        while (l0 > 1 && lv[l0 - 1].L.N <= thr) --l0;  // the finest level never joins the tail
+        if (l0 >= nsmooth() || (size_t)nlu * sizeof(T) > 200 * 1024) return 0;
+        const int nt = nsmooth() + 1 - l0;
+        std::vector<TailLevel<T>> h(nt);
+        for (int i = 0; i < nt; ++i) {
+            const Level<T>& L = lv[l0 + i];
+            h[i].L = L.L;
+            h[i].x[0] = L.x[0];
+            h[i].x[1] = L.x[1] ? L.x[1] : L.x[0];
+            h[i].b = L.b;
+            h[i].r = L.r;
+            h[i].sA = L.sA;
+            h[i].sM = L.sM;
+        }
+        if (int rc = dalloc(&tail_lv, (size_t)nt)) return rc;
+        CK(cudaMemcpy(tail_lv, h.data(), nt * sizeof(TailLevel<T>), cudaMemcpyHostToDevice));
+        tail_l = l0;
+        // upload the op lists of every possible entry (buffer a, zero start) now: nothing may
+        // allocate or copy while a cycle is being captured
+        for (int a = 0; a < 2; ++a)
+            for (int fz = 0; fz < 2; ++fz) {
+                std::vector<TailOp> ops;
+                tail_out[a][fz] = record(l0, a, fz != 0, ops);
+                if (int rc = dalloc(&tail_ops[a][fz], ops.size())) return rc;
+                CK(cudaMemcpy(tail_ops[a][fz], ops.data(), ops.size() * sizeof(TailOp), cudaMemcpyHostToDevice));
+                tail_nops[a][fz] = (int)ops.size();
+            }
+        return 0;
+    }
+
+    // the recursion of visit() (multigrid.py:157-185) recorded as tail ops (levels relative to tail_l)
+    int record(int l, int a, bool fz, std::vector<TailOp>& ops) {
+        const int rl = l - tail_l;
+        if (l == nsmooth()) {
+            ops.push_back(TailOp{TAIL_COARSE, rl, 0, 0, 0, 0});
+            return 0;
+        }
+        for (int k = 0; k < cfg.nu1; ++k) {
+            ops.push_back(TailOp{TAIL_SWEEP, rl, a, 1 - a, 0, fz ? 1 : 0});
+            a = 1 - a;
+            fz = false;
+        }
+        if (fz) ops.push_back(TailOp{TAIL_ZERO, rl, a, a, 0, 0});
+        ops.push_back(TailOp{TAIL_RESTRICT, rl, a, a, 0, 0});
+        int c;
+        if (l + 1 == nsmooth()) {
+            ops.push_back(TailOp{TAIL_COARSE, rl + 1, 0, 0, 0, 0});
+            c = 0;
+        } else {
+            c = record(l + 1, 0, true, ops);
+            for (int g = 1; g < cfg.gamma; ++g) c = record(l + 1, c, false, ops);
+        }
+        ops.push_back(TailOp{TAIL_PROLONG, rl, a, a, c, 0});
+        for (int k = 0; k < cfg.nu2; ++k) {
+            ops.push_back(TailOp{TAIL_SWEEP, rl, a, 1 - a, 0, 0});
+            a = 1 - a;
+        }
+        return a;
+    }
+
+    int tail_visit(int l, int a, bool fz, cudaStream_t s, int* launches) {
+        if (l != tail_l) return -1;
+        const int z = fz ? 1 : 0;
+        TailArgs<T> ta{};
+        ta.lv = tail_lv;
+        ta.ops = tail_ops[a][z];
+        ta.nops = tail_nops[a][z];
+        ta.M = M;
+        ta.omega = omega;
+        ta.lu = lu;
+        ta.piv = piv;
+        ta.nlu = nlu;
+        if (launch_tail<T>(ta, s) != cudaSuccess) return -1;
+        ++*launches;
+        return tail_out[a][z];
+    }
+
     // ||b - A x||_2 of the finest level appended to the device history
     int norm_launch(const T* x, cudaStream_t s, int* launches) {
         const Level<T>& L = lv[0];
@@ -547,6 +641,7 @@ template <class T> struct Solver final : spaimg_solver {
     // recursive schedule (multigrid.py:157-185).  Returns the buffer index of level l holding
     // the result, or -1 on error.  pre_done: the first pre-sweep of level 0 already ran (A).
     int visit(int l, int a, bool fz, cudaStream_t s, int* launches, bool pre_done) {
+        if (l >= tail_l && l < nsmooth()) return tail_visit(l, a, fz, s, launches);
         Level<T>& L = lv[l];
         if (l == nsmooth()) {  // u.N <= coarsest_N: direct solve (multigrid.py:166-167)
             if (launch_coarse_solve<T>(L.L, L.b, L.x[0], lu, piv, nlu, s) != cudaSuccess) return -1;

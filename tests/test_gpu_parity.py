@@ -223,6 +223,10 @@ def test_generic_stencils_vs_oracle(dim, N, dtype):
         got = host(sp.smooth(u, bb, M, om, 3))
         assert np.array_equal(got, c_oracle.smooth(x, b, N, mt, om, 3, dtype=npdt)), name
         if dtype == "float64":
-            cfg = sp.MgConfig(smoother=M, omega=om, cycle="V", nu1=1, nu2=1, coarsest_N=2)
-            got = host(sp.cycle(u, bb, cfg))
-            assert np.array_equal(got, c_oracle.cycle(x, b, N, mt, om, 1, 1, 1, 2)), name
+            Nc = 64 if dim == 2 else 32
+            xc = rng.uniform(-1, 1, (Nc - 1,) * dim)
+            bc = rng.uniform(-1, 1, (Nc - 1,) * dim)
+            for cyc, g in (("V", 1), ("W", 2)):
+                cfg = sp.MgConfig(smoother=M, omega=om, cycle=cyc, nu1=1, nu2=1, coarsest_N=2)
+                got = host(sp.cycle(sp.Grid(Nc, dev(xc)), sp.Grid(Nc, dev(bc)), cfg))
+                assert np.array_equal(got, c_oracle.cycle(xc, bc, Nc, mt, om, 1, 1, g, 2)), (name, cyc)
