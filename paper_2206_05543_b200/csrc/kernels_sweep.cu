@@ -351,7 +351,7 @@ bool sweep_fused_supported(int dim, int shape) {
 
 template <class T, int S, bool FZ, int NM>
 cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
-                                 T omega, const NormOut& no, cudaStream_t s);
+                                 T omega, const NormOut& no, cudaStream_t s, const Layout* Lc = nullptr);
 
 static bool sweep_v1() { return getenv("SPAIMG_SWEEP_V1") != nullptr; }
 bool sweep_norm_supported() { return !sweep_v1(); }
@@ -426,6 +426,10 @@ cudaError_t launch_residual_restrict(const Layout& Lf, const Layout& Lc, const T
                                      T* scratch_r, cudaStream_t s) {
     if (Lf.dim == 2 && !getenv("SPAIMG_RESTRICT_V1"))
         return launch_residual_restrict2d_march<T>(Lf, Lc, x, b, bc, sA, s);
+    if (Lf.dim == 3 && !getenv("SPAIMG_RESTRICT_V1")) {
+        const Terms<T> none{};
+        return launch_sweep3d_march<T, SHAPE_C1, false, 3>(Lf, x, b, bc, none, sA, T(0), T(0), NormOut{}, s, &Lc);
+    }
     cudaError_t e = launch_residual<T>(Lf, x, b, scratch_r, sA, s);
     if (e != cudaSuccess) return e;
     return launch_restrict<T>(Lf, Lc, scratch_r, bc, s);

@@ -54,7 +54,39 @@ struct M3Ctx {
     int n, x0, y0, q0, q_last, z0, z_end, yl, xl, tid;
     bool edge;  // tile touches the right/bottom boundary (masking needed)
     int cx, cy;  // TMA coordinates of the tile's stage origin (x stage)
+    // NM == 3 (K2 residual + restriction): coarse output level
+    T* cb;
+    long long cpx, cpp, corg;
+    int cm;
 };
+
+// K2 output of coarse plane I = (j-2)/2 from the r ring planes j-2, j-1, j: full weighting
+// along axis 0, then axis 1, then axis 2 (multigrid.py:104-119), the k_restrict tree.
+template <class T>
+__device__ __forceinline__ void m3_restrict_out(const M3Ctx<T>& c, int j, const T* r0, const T* r1, const T* r2) {
+    using G = M3<T>;
+    constexpr int CY = G::TY / 2, CX = G::TX / 2;
+    const int I = (j - 2) >> 1;
+#pragma unroll
+    for (int q0 = 0; q0 < CY * CX; q0 += M3_THREADS) {
+        const int q = q0 + c.tid;
+        const int yc = q / CX, xc = q % CX;
+        const int Y = (c.y0 >> 1) + yc, X = (c.x0 >> 1) + xc;
+        if (q >= CY * CX || Y >= c.cm || X >= c.cm) continue;
+        T u[3];
+#pragma unroll
+        for (int qk = 0; qk < 3; ++qk) {
+            T t[3];
+#pragma unroll
+            for (int qj = 0; qj < 3; ++qj) {
+                const int so = (2 * yc + qj + 1) * G::RW + G::VEC + 2 * xc + qk;
+                t[qj] = fw<T>(r2[so], r1[so], r0[so]);
+            }
+            u[qk] = fw<T>(t[0], t[1], t[2]);
+        }
+        c.cb[c.corg + (long long)I * c.cpp + (long long)Y * c.cpx + X] = fw<T>(u[0], u[1], u[2]);
+    }
+}
 
 template <class T, bool FZ>
 __device__ __forceinline__ void m3_issue(const M3Ctx<T>& c, const CUtensorMap* xm, const CUtensorMap* bm, int q,
@@ -97,7 +129,8 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
     constexpr int rj = P % M3_RR, rj1 = (P + 2) % M3_RR, rj2 = (P + 1) % M3_RR;  // r ring: planes j, j-1, j-2
     const int j = c.q0 + k;
     // generic shapes read r(j-3)'s ring slot in the previous step's output phase
-    if constexpr (S == SHAPE_GENERIC) __syncthreads();
+    // (NM == 3 reads r(j-3)'s slot as r(j-2) in its output phase)
+    if constexpr (S == SHAPE_GENERIC || NM == 3) __syncthreads();
     mbar_wait(&c.full[sp], (uint32_t)(((k + 1) / M3_ST) & 1));
     const bool plane_in = (unsigned)j < (unsigned)c.n;
 
@@ -137,7 +170,7 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
             for (int v = 0; v < VEC; ++v)
                 if (!plane_in || c.y0 + row >= c.n || c.x0 + c.xl + v >= c.n) R[ic][yy][v] = T(0);
         }
-        if (NM && j >= c.z0 && j < c.z_end) {
+        if ((NM == 1 || NM == 2) && j >= c.z0 && j < c.z_end) {
 #pragma unroll
             for (int v = 0; v < VEC; ++v) nacc += (double)R[ic][yy][v] * (double)R[ic][yy][v];
         }
@@ -170,6 +203,10 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
     }
     __syncthreads();
     if (c.tid == 0 && j - 1 + M3_ST <= c.q_last) m3_issue<T, FZ>(c, xmap, bmap, j - 1 + M3_ST, sm);
+    if constexpr (NM == 3) {
+        if ((j & 1) == 0 && j >= c.z0 + 1) m3_restrict_out<T>(c, j, c.rr + rj * G::RS, c.rr + rj1 * G::RS, c.rr + rj2 * G::RS);
+        return;
+    }
     if (NM == 2 || j - 1 < c.z0) return;
 
     // ---- output plane j-1 -------------------------------------------------------------------
@@ -233,7 +270,7 @@ template <class T, int S, bool FZ, int NM>
 __global__ void __launch_bounds__(M3_THREADS, 2)
     k_sweep3d_march(Layout L, const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap bmap,
                     const T* __restrict__ x, T* __restrict__ xo, Terms<T> M, T sA, T sM, T omega, int planes,
-                    NormOut no) {
+                    NormOut no, Layout Lc) {
     using G = M3<T>;
     constexpr int VEC = G::VEC;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -248,8 +285,19 @@ __global__ void __launch_bounds__(M3_THREADS, 2)
     c.pp = L.pp;
     c.x0 = blockIdx.x * G::TX;
     c.y0 = blockIdx.y * G::TY;
-    c.z0 = blockIdx.z * planes;
-    const int z_end = min(c.z0 + planes, c.n);
+    int z_end;
+    if constexpr (NM == 3) {  // chunk = coarse planes [z*planes, (z+1)*planes): fine r planes 2I0 .. 2I1
+        c.z0 = 2 * blockIdx.z * planes + 1;
+        z_end = min(2 * (blockIdx.z + 1) * planes, 2 * Lc.n);
+        c.cb = xo;
+        c.cpx = Lc.px;
+        c.cpp = Lc.pp;
+        c.corg = Lc.origin;
+        c.cm = Lc.n;
+    } else {
+        c.z0 = blockIdx.z * planes;
+        z_end = min(c.z0 + planes, c.n);
+    }
     c.z_end = z_end;
     c.q0 = c.z0 - 2;
     c.q_last = z_end + 1;
@@ -296,7 +344,7 @@ __global__ void __launch_bounds__(M3_THREADS, 2)
         M3STEP(6) M3STEP(7) M3STEP(8) M3STEP(9) M3STEP(10) M3STEP(11)
 #undef M3STEP
     }
-    if (NM) norm_epilogue(nacc, no);
+    if (NM == 1 || NM == 2) norm_epilogue(nacc, no);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -331,7 +379,7 @@ static cudaError_t make_map(CUtensorMap* map, const Layout& L, const T* base, in
 
 template <class T, int S, bool FZ, int NM>
 cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
-                                 T omega, const NormOut& no, cudaStream_t s) {
+                                 T omega, const NormOut& no, cudaStream_t s, const Layout* Lc) {
     using G = M3<T>;
     static bool attr = false;
     if (!attr) {
@@ -355,17 +403,19 @@ cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo,
     const int tx = (L.n + G::TX - 1) / G::TX, ty = (L.n + G::TY - 1) / G::TY;
     const int slots = num_sms() * occ;
     int chunks = std::max(1, (int)((2LL * slots + tx * ty - 1) / (tx * ty)));  // ~2 waves of marching CTAs
-    int planes = (L.n + chunks - 1) / chunks;
-    if (planes < 8) planes = 8;
-    chunks = (L.n + planes - 1) / planes;
+    const int span = NM == 3 ? Lc->n : L.n;  // NM == 3 chunks coarse planes
+    int planes = (span + chunks - 1) / chunks;
+    if (planes < (NM == 3 ? 4 : 8)) planes = NM == 3 ? 4 : 8;
+    chunks = (span + planes - 1) / planes;
     dim3 g(tx, ty, chunks);
-    k_sweep3d_march<T, S, FZ, NM><<<g, M3_THREADS, G::smem, s>>>(L, xm, bm, x, xo, M, sA, sM, omega, planes, no);
+    k_sweep3d_march<T, S, FZ, NM>
+        <<<g, M3_THREADS, G::smem, s>>>(L, xm, bm, x, xo, M, sA, sM, omega, planes, no, Lc ? *Lc : L);
     return cudaGetLastError();
 }
 
 #define SPAIMG_M3_INST(T, S, FZ, NM)                                                                           \
     template cudaError_t launch_sweep3d_march<T, S, FZ, NM>(const Layout&, const T*, const T*, T*, const Terms<T>&, \
-                                                            T, T, T, const NormOut&, cudaStream_t);
+                                                            T, T, T, const NormOut&, cudaStream_t, const Layout*);
 #define SPAIMG_M3_INST4(T, S) \
     SPAIMG_M3_INST(T, S, false, 0) SPAIMG_M3_INST(T, S, true, 0) SPAIMG_M3_INST(T, S, false, 1) SPAIMG_M3_INST(T, S, true, 1)
 SPAIMG_M3_INST4(double, SHAPE_GENERIC)
@@ -376,5 +426,7 @@ SPAIMG_M3_INST4(float, SHAPE_C1)
 SPAIMG_M3_INST4(float, SHAPE_STAR7)
 SPAIMG_M3_INST(double, SHAPE_C1, false, 2)
 SPAIMG_M3_INST(float, SHAPE_C1, false, 2)
+SPAIMG_M3_INST(double, SHAPE_C1, false, 3)
+SPAIMG_M3_INST(float, SHAPE_C1, false, 3)
 
 }  // namespace spaimg

@@ -186,7 +186,7 @@ static int alloc_level(Scratch& sc, Level<T>& lv, int dim, int N, bool two_x, bo
 }
 
 // kernel launches of one residual+restriction (2D: one fused marching kernel)
-static int residual_restrict_launches(int dim) { return dim == 2 && !getenv("SPAIMG_RESTRICT_V1") ? 1 : 2; }
+static int residual_restrict_launches(int) { return !getenv("SPAIMG_RESTRICT_V1") ? 1 : 2; }
 
 // one smoothing step on a level: x[a] -> x[1-a]
 template <class T>
@@ -501,7 +501,7 @@ template <class T> struct Solver final : spaimg_solver {
             if (int rc = dalloc(&l.b, (size_t)l.L.alloc)) return rc;
             if (!coarse) {
                 if (int rc = dalloc(&l.x[1], (size_t)l.L.alloc)) return rc;
-                if (!fused || c.dim == 3 || getenv("SPAIMG_RESTRICT_V1") || N <= tail_threshold(c))  // scratch r
+                if (!fused || getenv("SPAIMG_RESTRICT_V1") || N <= tail_threshold(c))  // scratch r
                     if (int rc = dalloc(&l.r, (size_t)l.L.alloc)) return rc;
             }
             lv.push_back(l);
