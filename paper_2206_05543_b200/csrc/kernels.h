@@ -42,6 +42,13 @@ cudaError_t launch_norm_march(const Layout& L, const T* x, const T* b, T sA, con
 template <class T>
 cudaError_t launch_residual_restrict(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T sA,
                                      T* scratch_r, cudaStream_t s);
+// K2 / K1 for small levels: flat one-wave kernels (kernels_flat.cu); levels with mesh count
+// N <= flat_threshold(dim) use them instead of the marching kernels
+int flat_threshold(int dim);
+template <class T>
+cudaError_t launch_residual_restrict_flat(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T sA,
+                                          cudaStream_t s);
+
 // K3: fused prolongation + correction xo = xi + P e (xi == xo allowed); acc=false stores P e alone
 template <class T>
 cudaError_t launch_prolong_correct(const Layout& Lf, const Layout& Lc, const T* xi, T* xo, const T* e, cudaStream_t s,

@@ -360,15 +360,16 @@ template <class T, int S, bool FZ, int NM>
 static cudaError_t sweep_dispatch(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
                                   T omega, const NormOut& no, cudaStream_t s) {
     constexpr int S3 = (S == SHAPE_GENERIC || S == SHAPE_C1 || S == SHAPE_STAR7) ? S : SHAPE_GENERIC;
+    const bool flat = NM == 0 && L.N <= flat_threshold(L.dim);
     if (L.dim == 2) {
-        if (sweep_v1() && NM == 0) {
+        if ((sweep_v1() || flat) && NM == 0) {
             dim3 g((L.n + S2_TW - 1) / S2_TW, (L.n + S2_TH - 1) / S2_TH);
             k_sweep2d_tile<T, S, FZ><<<g, 256, 0, s>>>(L, x, b, xo, M, sA, sM, omega);
             return cudaGetLastError();
         }
         return launch_sweep2d_march<T, S, FZ, NM>(L, x, b, xo, M, sA, sM, omega, no, s);
     }
-    if (sweep_v1() && NM == 0) {
+    if ((sweep_v1() || flat) && NM == 0) {
         dim3 g((L.n + S3_TX - 1) / S3_TX, (L.n + S3_TY - 1) / S3_TY, (L.n + S3_TZ - 1) / S3_TZ);
         k_sweep3d_tile<T, S, FZ><<<g, 256, 0, s>>>(L, x, b, xo, M, sA, sM, omega);
         return cudaGetLastError();
@@ -424,6 +425,8 @@ cudaError_t launch_residual_restrict2d_march(const Layout& Lf, const Layout& Lc,
 template <class T>
 cudaError_t launch_residual_restrict(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T sA,
                                      T* scratch_r, cudaStream_t s) {
+    if (Lf.N <= flat_threshold(Lf.dim) && !getenv("SPAIMG_RESTRICT_V1"))
+        return launch_residual_restrict_flat<T>(Lf, Lc, x, b, bc, sA, s);
     if (Lf.dim == 2 && !getenv("SPAIMG_RESTRICT_V1"))
         return launch_residual_restrict2d_march<T>(Lf, Lc, x, b, bc, sA, s);
     if (Lf.dim == 3 && !getenv("SPAIMG_RESTRICT_V1")) {
