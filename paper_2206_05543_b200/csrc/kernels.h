@@ -7,6 +7,24 @@
 
 namespace spaimg {
 
+// launch with the Programmatic-Dependent-Launch attribute when SPAIMG_PDL=1; the kernel
+// must call pdl_wait() before its first global memory access
+bool pdl_enabled();
+template <class... KP, class... A>
+inline cudaError_t launch_pdl(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KP>(args)...);
+}
+
 Layout make_layout(int dim, int N, int esize);
 
 // dense (n^dim, C order) <-> padded interior
@@ -65,32 +83,41 @@ template <class T>
 cudaError_t launch_coarse_solve(const Layout& L, const T* b, T* x, const T* lu, const int* piv, int nlu,
                                 cudaStream_t s);
 
-// K5+: single-block tail of the cycle (kernels_tail.cu): every level from a threshold down
-// runs inside one CTA, interpreting the host-recorded op list of the recursion.
+// K5+: single-block, shared-memory-resident tail of the cycle (kernels_tail.cu): every level
+// from a threshold down runs inside one CTA, interpreting the host-recorded op list of the
+// recursion (levels relative to the entry level 0).
 enum TailOpType { TAIL_SWEEP = 0, TAIL_ZERO = 1, TAIL_RESTRICT = 2, TAIL_PROLONG = 3, TAIL_COARSE = 4 };
 struct TailOp {
     int type;
-    int level;  // index into TailArgs::lv
+    int level;        // index into the tail levels (0 = entry level)
     int a_in, a_out;  // x buffer indices of the level
     int c;            // PROLONG: x buffer of the coarse level holding the correction
     int fz;           // SWEEP: the input iterate is zero (x not read)
 };
 template <class T> struct TailLevel {
-    Layout L;
-    T* x[2];
+    Layout L;   // compact shared-memory layout (frame = stencil radius)
+    T* x[2];    // host side: element offsets into the shared array block
     T* b;
     T* r;
     T sA, sM;
 };
 template <class T> struct TailArgs {
-    const TailLevel<T>* lv;  // device array
-    const TailOp* ops;       // device array
-    int nops;
+    const TailLevel<T>* lv;  // device array, nlv entries
+    const TailOp* ops;       // device array, nops entries
+    int nlv, nops;
+    size_t arr_off;          // byte offset of the level arrays in shared memory
+    int arr_elems;           // elements of all level arrays (y follows them)
+    size_t smem;             // dynamic shared memory bytes
     Terms<T> M;
     T omega;
     const T* lu;
     const int* piv;
     int nlu;
+    Layout gL;               // entry level in global memory
+    const T* gb;
+    const T* gx_in;          // start iterate (entry_fz == 0)
+    T* gx_out;               // result iterate
+    int entry_fz, entry_a, out_a;
 };
 template <class T> cudaError_t launch_tail(const TailArgs<T>& a, cudaStream_t s);
 

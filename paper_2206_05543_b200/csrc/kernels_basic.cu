@@ -238,6 +238,8 @@ template <class T>
 __global__ void __launch_bounds__(128) k_prolong_correct2d(Layout Lf, Layout Lc, const T* xi, T* xo,
                                                            const T* __restrict__ e, bool acc) {
     using O = Op<T>;
+    pdl_wait();
+    pdl_trigger();
     const int m = Lc.n;
     const int J = blockIdx.x * blockDim.x + threadIdx.x;
     const int I = blockIdx.y;
@@ -287,6 +289,8 @@ template <class T>
 __global__ void __launch_bounds__(128) k_prolong_correct3d(Layout Lf, Layout Lc, const T* xi, T* xo,
                                                            const T* __restrict__ e, bool acc) {
     using O = Op<T>;
+    pdl_wait();
+    pdl_trigger();
     const int m = Lc.n;
     const int K = blockIdx.x * blockDim.x + threadIdx.x;
     const int J = blockIdx.y, I = blockIdx.z;
@@ -350,10 +354,10 @@ cudaError_t launch_prolong_correct(const Layout& Lf, const Layout& Lc, const T* 
     const int m = Lc.n;
     if (Lf.dim == 2) {
         dim3 g((m + 1 + 127) / 128, m + 1);
-        k_prolong_correct2d<T><<<g, 128, 0, s>>>(Lf, Lc, xi, xo, e, acc);
+        return launch_pdl(k_prolong_correct2d<T>, g, dim3(128), 0, s, Lf, Lc, xi, xo, e, acc);
     } else {
         dim3 g((m + 1 + 127) / 128, m + 1, m + 1);
-        k_prolong_correct3d<T><<<g, 128, 0, s>>>(Lf, Lc, xi, xo, e, acc);
+        return launch_pdl(k_prolong_correct3d<T>, g, dim3(128), 0, s, Lf, Lc, xi, xo, e, acc);
     }
     return cudaGetLastError();
 }
@@ -445,6 +449,8 @@ __global__ void k_coarse_solve(Layout L, const T* __restrict__ b, T* __restrict_
     using O = Op<T>;
     extern __shared__ unsigned char smem_raw[];
     T* y = reinterpret_cast<T*>(smem_raw);
+    pdl_wait();
+    pdl_trigger();
     const int n = L.n;
     for (int q = threadIdx.x; q < nlu; q += blockDim.x) {
         const int i0 = L.dim == 2 ? q / n : q / (n * n);
@@ -492,8 +498,7 @@ cudaError_t launch_coarse_solve(const Layout& L, const T* b, T* x, const T* lu, 
         cudaError_t e = cudaFuncSetAttribute(k_coarse_solve<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    k_coarse_solve<T><<<1, 256, smem, s>>>(L, b, x, lu, piv, nlu);
-    return cudaGetLastError();
+    return launch_pdl(k_coarse_solve<T>, dim3(1), dim3(256), smem, s, L, b, x, lu, piv, nlu);
 }
 
 // ------------------------------------------------------------------------------------------

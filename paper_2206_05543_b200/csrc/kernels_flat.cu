@@ -22,6 +22,8 @@ __global__ void __launch_bounds__(256) k_rr2d_flat(Layout Lf, Layout Lc, const T
                                                    const T* __restrict__ b, T* __restrict__ bc, T sA) {
     constexpr int RH = 2 * F2_CH + 1, RW = 2 * F2_CW + 1, RP = RW + 1;
     __shared__ T rs[RH * RP];
+    pdl_wait();
+    pdl_trigger();
     const int n = Lf.n, m = Lc.n;
     const int I0 = blockIdx.y * F2_CH, J0 = blockIdx.x * F2_CW;
     const int f0 = 2 * I0, g0 = 2 * J0;  // fine interior index of local (0, 0)
@@ -53,6 +55,8 @@ __global__ void __launch_bounds__(256) k_rr3d_flat(Layout Lf, Layout Lc, const T
                                                    const T* __restrict__ b, T* __restrict__ bc, T sA) {
     constexpr int RZ = 2 * F3_CZ + 1, RY = 2 * F3_CY + 1, RX = 2 * F3_CX + 1, RP = RX + 1;
     __shared__ T rs[RZ * RY * RP];
+    pdl_wait();
+    pdl_trigger();
     const int n = Lf.n, m = Lc.n;
     const int I0 = blockIdx.z * F3_CZ, J0 = blockIdx.y * F3_CY, K0 = blockIdx.x * F3_CX;
     const int f0 = 2 * I0, f1 = 2 * J0, f2 = 2 * K0;
@@ -85,6 +89,17 @@ __global__ void __launch_bounds__(256) k_rr3d_flat(Layout Lf, Layout Lc, const T
     bc[Lc.origin + (long long)I * Lc.pp + (long long)J * Lc.px + K] = fw<T>(u[0], u[1], u[2]);
 }
 
+bool pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        // measured neutral-to-slightly-negative on the c1-c4 cycles (launch latency is not the
+        // bottleneck of the small levels; their memory latency is), so opt-in
+        const char* e = getenv("SPAIMG_PDL");
+        on = (e && e[0] == '1') ? 1 : 0;
+    }
+    return on == 1;
+}
+
 int flat_threshold(int dim) {
     const char* e = getenv(dim == 2 ? "SPAIMG_FLAT_N2" : "SPAIMG_FLAT_N3");
     if (e) return atoi(e);
@@ -97,10 +112,10 @@ cudaError_t launch_residual_restrict_flat(const Layout& Lf, const Layout& Lc, co
     const int m = Lc.n;
     if (Lf.dim == 2) {
         dim3 g((m + F2_CW - 1) / F2_CW, (m + F2_CH - 1) / F2_CH);
-        k_rr2d_flat<T><<<g, 256, 0, s>>>(Lf, Lc, x, b, bc, sA);
+        return launch_pdl(k_rr2d_flat<T>, g, dim3(256), 0, s, Lf, Lc, x, b, bc, sA);
     } else {
         dim3 g((m + F3_CX - 1) / F3_CX, (m + F3_CY - 1) / F3_CY, (m + F3_CZ - 1) / F3_CZ);
-        k_rr3d_flat<T><<<g, 256, 0, s>>>(Lf, Lc, x, b, bc, sA);
+        return launch_pdl(k_rr3d_flat<T>, g, dim3(256), 0, s, Lf, Lc, x, b, bc, sA);
     }
     return cudaGetLastError();
 }

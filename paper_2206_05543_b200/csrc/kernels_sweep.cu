@@ -28,6 +28,8 @@ __global__ void __launch_bounds__(256) k_sweep2d_tile(Layout L, const T* __restr
     using O = Op<T>;
     constexpr int RW = S2_TW + 2, RH = S2_TH + 2;
     __shared__ T rs[RH * RW];
+    pdl_wait();
+    pdl_trigger();
     const int c0 = blockIdx.x * S2_TW, r0 = blockIdx.y * S2_TH;
     const int n = L.n;
     for (int q = threadIdx.x; q < RH * RW; q += blockDim.x) {
@@ -67,6 +69,8 @@ __global__ void __launch_bounds__(256) k_sweep3d_tile(Layout L, const T* __restr
     using O = Op<T>;
     constexpr int RX = S3_TX + 2, RY = S3_TY + 2, RZ = S3_TZ + 2;
     __shared__ T rs[RZ * RY * RX];
+    pdl_wait();
+    pdl_trigger();
     const int x0 = blockIdx.x * S3_TX, y0 = blockIdx.y * S3_TY, z0 = blockIdx.z * S3_TZ;
     const int n = L.n;
     for (int q = threadIdx.x; q < RZ * RY * RX; q += blockDim.x) {
@@ -265,6 +269,8 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, co
     constexpr int RW = m2_rowlen<T>();
     constexpr int ST = M2_ST;
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    pdl_wait();
+    pdl_trigger();
     M2Ctx<T> c;
     c.xs = reinterpret_cast<T*>(smem_raw);
     c.bs = c.xs + ST * RW;
@@ -340,8 +346,8 @@ static cudaError_t launch_sweep2d_march(const Layout& L, const T* x, const T* b,
     if (rows < 16) rows = 16;
     chunks = (L.n + rows - 1) / rows;
     dim3 g(strips, chunks);
-    k_sweep2d_march<T, S, FZ, NM><<<g, threads, smem, s>>>(L, x, b, xo, M, sA, sM, omega, rows, no);
-    return cudaGetLastError();
+    return launch_pdl(k_sweep2d_march<T, S, FZ, NM>, g, dim3(threads), smem, s, L, x, b, xo, M, sA, sM, omega, rows,
+                      no);
 }
 
 bool sweep_fused_supported(int dim, int shape) {
@@ -364,15 +370,13 @@ static cudaError_t sweep_dispatch(const Layout& L, const T* x, const T* b, T* xo
     if (L.dim == 2) {
         if ((sweep_v1() || flat) && NM == 0) {
             dim3 g((L.n + S2_TW - 1) / S2_TW, (L.n + S2_TH - 1) / S2_TH);
-            k_sweep2d_tile<T, S, FZ><<<g, 256, 0, s>>>(L, x, b, xo, M, sA, sM, omega);
-            return cudaGetLastError();
+            return launch_pdl(k_sweep2d_tile<T, S, FZ>, g, dim3(256), 0, s, L, x, b, xo, M, sA, sM, omega);
         }
         return launch_sweep2d_march<T, S, FZ, NM>(L, x, b, xo, M, sA, sM, omega, no, s);
     }
     if ((sweep_v1() || flat) && NM == 0) {
         dim3 g((L.n + S3_TX - 1) / S3_TX, (L.n + S3_TY - 1) / S3_TY, (L.n + S3_TZ - 1) / S3_TZ);
-        k_sweep3d_tile<T, S, FZ><<<g, 256, 0, s>>>(L, x, b, xo, M, sA, sM, omega);
-        return cudaGetLastError();
+        return launch_pdl(k_sweep3d_tile<T, S, FZ>, g, dim3(256), 0, s, L, x, b, xo, M, sA, sM, omega);
     }
     return launch_sweep3d_march<T, S3, FZ, NM>(L, x, b, xo, M, sA, sM, omega, no, s);
 }

@@ -1,15 +1,21 @@
-// K5+: single-block coarse-level path.  All levels at or below a size threshold -- every
-// smoothing sweep, residual + restriction, the coarse direct solve and every prolongation +
-// correction of the tail of the V/W recursion (reference multigrid.py:157-185) -- run inside
-// ONE CTA of 1024 threads, phase after phase separated by __syncthreads(), instead of one
-// graph node per operation.  The host walks the same recursion as the multi-kernel schedule
-// and records it as a list of TailOps; the kernel interprets that list.
+// K5+: single-block, shared-memory-resident tail of the cycle.  Every operation of the V/W
+// recursion (reference multigrid.py:157-185) on the levels at or below a size threshold --
+// smoothing sweeps, residual + restriction, the coarse direct solve, prolongation + correction
+// -- runs inside ONE CTA of 1024 threads, instead of ~4 dependent graph nodes per level (each
+// several microseconds of launch + memory latency for well under a microsecond of work).
 //
-// Data stays in the levels' own padded buffers (global memory, L1/L2 resident at these
-// sizes: 2D N<=64 is <= 32 KB of interior per vector).  All loads are plain (coherent) loads:
-// after __syncthreads() every write of the block is visible to the block, which is the only
-// ordering the schedule needs.  Every per-point expression is the same Appendix-A tree as the
-// multi-kernel path (spaimg_common.cuh), so the tail is bitwise identical to it.
+// The host walks the same recursion as the multi-kernel schedule and records it as a list of
+// TailOps.  The kernel
+//   1. copies the op list and the level descriptors into shared memory,
+//   2. zeroes the tail levels' compact shared-memory arrays (frame F = stencil radius: the
+//      zero frame is the reference's zero extension, stencils.py:139-146),
+//   3. loads the entry level's b (and x unless the entry starts from zero) from its global
+//      level buffers,
+//   4. interprets the ops, phases separated by __syncthreads(),
+//   5. stores the entry level's resulting x back to its global buffer (the caller's
+//      prolongation reads it there).
+// Every per-point expression is the Appendix-A tree of the multi-kernel path
+// (spaimg_common.cuh), so the tail is bitwise identical to it; only the memory changes.
 #include "kernels.h"
 #include "march.cuh"
 
@@ -29,6 +35,8 @@ __device__ __forceinline__ long long tpoint(const Layout& L, int q) {
     return L.origin + (long long)i0 * L.pp + (long long)(rem / n) * L.px + (rem % n);
 }
 
+__device__ __forceinline__ int npoints(const Layout& L) { return L.dim == 2 ? L.n * L.n : L.n * L.n * L.n; }
+
 template <class T>
 __device__ __forceinline__ T tail_residual(const Layout& L, const T* x, const T* b, long long p, T sA) {
     if (L.dim == 2) return residual2d<T>(b[p], x[p], x[p + L.px], x[p - L.px], x[p + 1], x[p - 1], sA);
@@ -39,7 +47,7 @@ __device__ __forceinline__ T tail_residual(const Layout& L, const T* x, const T*
 template <class T>
 __device__ void tail_residual_phase(const TailLevel<T>& v, const T* x, bool fz) {
     const Layout& L = v.L;
-    const int cnt = L.dim == 2 ? L.n * L.n : L.n * L.n * L.n;
+    const int cnt = npoints(L);
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
         const long long p = tpoint(L, q);
         v.r[p] = fz ? v.b[p] : tail_residual<T>(L, x, v.b, p, v.sA);
@@ -51,7 +59,7 @@ template <class T>
 __device__ void tail_relax_phase(const TailLevel<T>& v, const T* x, T* xo, const Terms<T>& M, T omega) {
     using O = Op<T>;
     const Layout& L = v.L;
-    const int cnt = L.dim == 2 ? L.n * L.n : L.n * L.n * L.n;
+    const int cnt = npoints(L);
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
         const long long p = tpoint(L, q);
         T acc = T(0);
@@ -70,7 +78,7 @@ __device__ void tail_restrict_phase(const TailLevel<T>& f, const TailLevel<T>& c
     const Layout& Lf = f.L;
     const Layout& Lc = c.L;
     const int m = Lc.n;
-    const int cnt = Lf.dim == 2 ? m * m : m * m * m;
+    const int cnt = npoints(Lc);
     const T* r = f.r;
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
         if (Lf.dim == 2) {
@@ -116,7 +124,7 @@ __device__ void tail_prolong_phase(const TailLevel<T>& f, const TailLevel<T>& c,
     const Layout& Lf = f.L;
     const Layout& Lc = c.L;
     const int m = Lc.n;
-    const int cnt = Lf.dim == 2 ? Lf.n * Lf.n : Lf.n * Lf.n * Lf.n;
+    const int cnt = npoints(Lf);
     const int n = Lf.n;
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
         T val;
@@ -125,9 +133,7 @@ __device__ void tail_prolong_phase(const TailLevel<T>& f, const TailLevel<T>& c,
             const int i0 = q / n, i1 = q % n;
             p = tidx(Lf, i0, i1, 0);
             // axis 0 at fine row i0 for coarse column j1, then axis 1
-            auto t0 = [&](int j1) {
-                return tail_interp<T>(i0, m, [&](int j0) { return e[tidx(Lc, j0, j1, 0)]; });
-            };
+            auto t0 = [&](int j1) { return tail_interp<T>(i0, m, [&](int j0) { return e[tidx(Lc, j0, j1, 0)]; }); };
             val = tail_interp<T>(i1, m, t0);
         } else {
             const int i0 = q / (n * n), i1 = (q / n) % n, i2 = q % n;
@@ -177,13 +183,40 @@ __device__ void tail_coarse_phase(const TailLevel<T>& v, T* y, const T* lu, cons
     for (int q = threadIdx.x; q < nlu; q += blockDim.x) v.x[0][tpoint(L, q)] = y[q];
 }
 
+// copy the interior of one level between two layouts (global padded <-> shared compact)
+template <class T>
+__device__ void tail_copy(const Layout& Ld, T* dst, const Layout& Ls, const T* src) {
+    const int cnt = npoints(Ld);
+    for (int q = threadIdx.x; q < cnt; q += blockDim.x) dst[tpoint(Ld, q)] = src[tpoint(Ls, q)];
+}
+
 template <class T>
 __global__ void __launch_bounds__(kTailThreads) k_tail(TailArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* y = reinterpret_cast<T*>(smem_raw);
+    pdl_wait();
+    pdl_trigger();
+    // [level descriptors | ops | level arrays | LU work vector y]
+    TailLevel<T>* lv = reinterpret_cast<TailLevel<T>*>(smem_raw);
+    TailOp* ops = reinterpret_cast<TailOp*>(lv + a.nlv);
+    T* arr = reinterpret_cast<T*>(smem_raw + a.arr_off);
+    T* y = arr + a.arr_elems;
+    for (int i = threadIdx.x; i < a.nlv; i += blockDim.x) {
+        TailLevel<T> v = a.lv[i];  // host-built: the array "pointers" are element offsets into arr
+        for (int k = 0; k < 2; ++k) v.x[k] = arr + reinterpret_cast<size_t>(v.x[k]);
+        v.b = arr + reinterpret_cast<size_t>(v.b);
+        v.r = arr + reinterpret_cast<size_t>(v.r);
+        lv[i] = v;
+    }
+    for (int i = threadIdx.x; i < a.nops; i += blockDim.x) ops[i] = a.ops[i];
+    for (int i = threadIdx.x; i < a.arr_elems; i += blockDim.x) arr[i] = T(0);
+    __syncthreads();
+    // entry level: b (and the start iterate) from its global buffers
+    tail_copy<T>(lv[0].L, lv[0].b, a.gL, a.gb);
+    if (!a.entry_fz) tail_copy<T>(lv[0].L, lv[0].x[a.entry_a], a.gL, a.gx_in);
     for (int i = 0; i < a.nops; ++i) {
-        const TailOp op = a.ops[i];
-        const TailLevel<T>& v = a.lv[op.level];
+        __syncthreads();
+        const TailOp op = ops[i];
+        const TailLevel<T>& v = lv[op.level];
         switch (op.type) {
             case TAIL_SWEEP:
                 tail_residual_phase<T>(v, v.x[op.a_in], op.fz);
@@ -191,18 +224,17 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(TailArgs<T> a) {
                 tail_relax_phase<T>(v, op.fz ? nullptr : v.x[op.a_in], v.x[op.a_out], a.M, a.omega);
                 break;
             case TAIL_ZERO: {
-                const Layout& L = v.L;
-                const int cnt = L.dim == 2 ? L.n * L.n : L.n * L.n * L.n;
-                for (int q = threadIdx.x; q < cnt; q += blockDim.x) v.x[op.a_out][tpoint(L, q)] = T(0);
+                const int cnt = npoints(v.L);
+                for (int q = threadIdx.x; q < cnt; q += blockDim.x) v.x[op.a_out][tpoint(v.L, q)] = T(0);
                 break;
             }
             case TAIL_RESTRICT:
                 tail_residual_phase<T>(v, v.x[op.a_in], false);
                 __syncthreads();
-                tail_restrict_phase<T>(v, a.lv[op.level + 1]);
+                tail_restrict_phase<T>(v, lv[op.level + 1]);
                 break;
             case TAIL_PROLONG: {
-                const TailLevel<T>& c = a.lv[op.level + 1];
+                const TailLevel<T>& c = lv[op.level + 1];
                 tail_prolong_phase<T>(v, c, v.x[op.a_in], v.x[op.a_out], c.x[op.c]);
                 break;
             }
@@ -210,19 +242,20 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(TailArgs<T> a) {
                 tail_coarse_phase<T>(v, y, a.lu, a.piv, a.nlu);
                 break;
         }
-        __syncthreads();
     }
+    __syncthreads();
+    tail_copy<T>(a.gL, a.gx_out, lv[0].L, lv[0].x[a.out_a]);
 }
 
 template <class T>
 cudaError_t launch_tail(const TailArgs<T>& a, cudaStream_t s) {
-    const size_t smem = (size_t)(a.nlu > 0 ? a.nlu : 1) * sizeof(T);
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k_tail<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static size_t attr = 0;
+    if (a.smem > 48 * 1024 && a.smem > attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_tail<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem);
         if (e != cudaSuccess) return e;
+        attr = a.smem;
     }
-    k_tail<T><<<1, kTailThreads, smem, s>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(k_tail<T>, dim3(1), dim3(kTailThreads), a.smem, s, a);
 }
 
 template cudaError_t launch_tail<double>(const TailArgs<double>&, cudaStream_t);

@@ -1,6 +1,7 @@
 // C-ABI entry points (include/spaimg_cuda.h) and the native multigrid runtime: the padded
 // level hierarchy, the V/W-cycle schedule (reference multigrid.py:157-185) captured into a
 // CUDA graph, and the solve loop (multigrid.py:203-219).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -9,6 +10,7 @@
 #include <vector>
 
 #include "kernels.h"
+#include "march.cuh"
 #include "spaimg_cuda.h"
 
 using namespace spaimg;
@@ -402,6 +404,8 @@ struct SolveCtl {
 };
 
 __global__ void k_solve_reset(int* slot, int* state) {
+    pdl_wait();
+    pdl_trigger();
     *slot = 0;
     state[0] = 0;
     state[1] = 0;
@@ -409,6 +413,8 @@ __global__ void k_solve_reset(int* slot, int* state) {
 
 __global__ void k_solve_check(const double* norms, const int* slot, const SolveCtl* ctl, int* state,
                               cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hi) {
+    pdl_wait();
+    pdl_trigger();
     const int k = *slot - 1;  // norms[0..k] are known: k cycles done
     const bool conv = k >= 1 && norms[k] <= ctl->tol * norms[0];
     const bool cont = !conv && k < ctl->max_iters;
@@ -449,12 +455,14 @@ template <class T> struct Solver final : spaimg_solver {
     bool use_graph = true;
     std::vector<void*> owned;
     std::vector<std::pair<long long, cudaGraphExec_t>> op_graphs;
-    // single-block tail: levels >= tail_l (if < nsmooth()) run in one CTA per visit
+    // single-block shared-memory tail: levels >= tail_l (if < nsmooth()) run in one CTA per visit
     int tail_l = 1 << 30;
-    TailLevel<T>* tail_lv = nullptr;               // device copy of the tail levels' descriptors
-    TailOp* tail_ops[2][2] = {};  // uploaded op lists keyed by (entry buffer a, zero start)
+    TailLevel<T>* tail_lv = nullptr;  // device copy of the tail levels' shared-memory descriptors
+    TailOp* tail_ops[2][2] = {};      // uploaded op lists keyed by (entry buffer a, zero start)
     int tail_nops[2][2] = {};
     int tail_out[2][2] = {};
+    int tail_nlv = 0, tail_elems = 0;
+    size_t tail_arr_off = 0, tail_smem = 0;
 
     ~Solver() override {
         if (exec_cycle) cudaGraphExecDestroy(exec_cycle);
@@ -539,33 +547,85 @@ template <class T> struct Solver final : spaimg_solver {
 
     int nsmooth() const { return (int)lv.size() - 1; }
 
-    // largest mesh count run by the single-block tail (SPAIMG_TAIL_N overrides; 0 disables)
+    // largest mesh count run by the shared-memory tail kernel (SPAIMG_TAIL_N overrides; 0 disables)
     static int tail_threshold(const spaimg_mg_config& c) {
         const char* e = getenv("SPAIMG_TAIL_N");
         if (e) return atoi(e);
-        return c.dim == 2 ? 32 : 8;  // measured optimum (tools/tune.py, c1/c2/c4)
+        return c.dim == 2 ? 32 : 8;  // measured optimum (tools/tune.py c1-c4)
+    }
+
+    // compact shared-memory layout of an n^dim level with a zero frame of F cells
+    static Layout smem_layout(int dim, int N, int F) {
+        Layout L{};
+        L.dim = dim;
+        L.N = N;
+        L.n = N - 1;
+        L.esize = sizeof(T);
+        const long long w = L.n + 2 * F;
+        L.px = w;
+        L.pp = dim == 3 ? w * w : 0;
+        L.origin = dim == 3 ? F * L.pp + F * w + F : F * w + F;
+        L.alloc = dim == 3 ? w * w * w : w * w;
+        return L;
     }
 
     int init_tail() {
         const int thr = tail_threshold(cfg);
+        if (thr <= 0) return 0;
+        const int F = std::max(1, stencil_radius(cfg.M));
+        int dev = 0, optin = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         int l0 = nsmooth();
         while (l0 > 1 && lv[l0 - 1].L.N <= thr) --l0;  // the finest level never joins the tail
-        if (l0 >= nsmooth() || (size_t)nlu * sizeof(T) > 200 * 1024) return 0;
-        const int nt = nsmooth() + 1 - l0;
-        std::vector<TailLevel<T>> h(nt);
-        for (int i = 0; i < nt; ++i) {
-            const Level<T>& L = lv[l0 + i];
-            h[i].L = L.L;
-            h[i].x[0] = L.x[0];
-            h[i].x[1] = L.x[1] ? L.x[1] : L.x[0];
-            h[i].b = L.b;
-            h[i].r = L.r;
-            h[i].sA = L.sA;
-            h[i].sM = L.sM;
+        std::vector<TailLevel<T>> h;
+        size_t arr_off = 0;
+        int elems = 0;
+        // shrink the tail until its levels fit in one CTA's shared memory
+        for (; l0 < nsmooth(); ++l0) {
+            const int nt = nsmooth() + 1 - l0;
+            h.assign(nt, TailLevel<T>{});
+            elems = 0;
+            for (int i = 0; i < nt; ++i) {
+                const Level<T>& L = lv[l0 + i];
+                const bool coarse = l0 + i == nsmooth();
+                h[i].L = smem_layout(cfg.dim, L.L.N, F);
+                const int a = (int)h[i].L.alloc;
+                auto take = [&](int cnt) { T* p = reinterpret_cast<T*>((size_t)elems); elems += cnt; return p; };
+                h[i].x[0] = take(a);
+                h[i].x[1] = coarse ? h[i].x[0] : take(a);
+                h[i].b = take(a);
+                h[i].r = coarse ? h[i].b : take(a);
+                h[i].sA = L.sA;
+                h[i].sM = L.sM;
+            }
+            // descriptors + the longest op list (W: every visit is recorded) precede the arrays
+            size_t nops_max = 0;
+            {
+                const int save = tail_l;
+                tail_l = l0;
+                for (int a = 0; a < 2; ++a) {
+                    std::vector<TailOp> ops;
+                    record(l0, a, a == 0, ops);
+                    nops_max = std::max(nops_max, ops.size());
+                }
+                tail_l = save;
+            }
+            arr_off = (nt * sizeof(TailLevel<T>) + nops_max * sizeof(TailOp) + 15) / 16 * 16;
+            const size_t smem = arr_off + ((size_t)elems + nlu) * sizeof(T);
+            if (smem <= (size_t)optin) {
+                tail_smem = smem;
+                break;
+            }
         }
+        if (l0 >= nsmooth()) return 0;
+        const int nt = nsmooth() + 1 - l0;
         if (int rc = dalloc(&tail_lv, (size_t)nt)) return rc;
         CK(cudaMemcpy(tail_lv, h.data(), nt * sizeof(TailLevel<T>), cudaMemcpyHostToDevice));
         tail_l = l0;
+        tail_nlv = nt;
+        tail_elems = elems;
+        tail_arr_off = arr_off;
         // upload the op lists of every possible entry (buffer a, zero start) now: nothing may
         // allocate or copy while a cycle is being captured
         for (int a = 0; a < 2; ++a)
@@ -612,18 +672,30 @@ template <class T> struct Solver final : spaimg_solver {
     int tail_visit(int l, int a, bool fz, cudaStream_t s, int* launches) {
         if (l != tail_l) return -1;
         const int z = fz ? 1 : 0;
+        const Level<T>& G = lv[l];
         TailArgs<T> ta{};
         ta.lv = tail_lv;
         ta.ops = tail_ops[a][z];
+        ta.nlv = tail_nlv;
         ta.nops = tail_nops[a][z];
+        ta.arr_off = tail_arr_off;
+        ta.arr_elems = tail_elems;
+        ta.smem = tail_smem;
         ta.M = M;
         ta.omega = omega;
         ta.lu = lu;
         ta.piv = piv;
         ta.nlu = nlu;
+        ta.gL = G.L;
+        ta.gb = G.b;
+        ta.gx_in = G.x[a];
+        ta.out_a = tail_out[a][z];
+        ta.gx_out = G.x[ta.out_a];
+        ta.entry_fz = z;
+        ta.entry_a = a;
         if (launch_tail<T>(ta, s) != cudaSuccess) return -1;
         ++*launches;
-        return tail_out[a][z];
+        return ta.out_a;
     }
 
     // ||b - A x||_2 of the finest level appended to the device history
@@ -749,8 +821,7 @@ template <class T> struct Solver final : spaimg_solver {
         if (e != cudaSuccess) rc = fail((int)e, "conditional handle");
         if (!rc)
             rc = capture_into(g, [&](cudaStream_t cs) -> int {
-                k_solve_reset<<<1, 1, 0, cs>>>(slot_d, state_d);
-                CK(cudaGetLastError());
+                CK(launch_pdl(k_solve_reset, dim3(1), dim3(1), 0, cs, slot_d, state_d));
                 return add_conditional(cs, hw, cudaGraphCondTypeWhile, &wbody);
             });
         if (!rc) {
@@ -760,8 +831,7 @@ template <class T> struct Solver final : spaimg_solver {
         if (!rc)
             rc = capture_into(wbody, [&](cudaStream_t cs) -> int {
                 if (int r = part_a(cs, &launches_a)) return r;
-                k_solve_check<<<1, 1, 0, cs>>>(norms_d, slot_d, ctl_d, state_d, hw, hi);
-                CK(cudaGetLastError());
+                CK(launch_pdl(k_solve_check, dim3(1), dim3(1), 0, cs, norms_d, slot_d, ctl_d, state_d, hw, hi));
                 ++launches_a;
                 return add_conditional(cs, hi, cudaGraphCondTypeIf, &ibody);
             });
