@@ -51,6 +51,11 @@ template <class T>
 cudaError_t launch_sweep(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, int shape, T sA,
                          T sM, T omega, bool from_zero, cudaStream_t s, const NormOut* no = nullptr);
 bool sweep_fused_supported(int dim, int shape);
+// K3 + K1: xo = sweep(x + P e) (prolongation + correction fused into the first post-sweep)
+bool sweep_pc_supported(const Layout& L);
+template <class T>
+cudaError_t launch_sweep_pc(const Layout& L, const Layout& Lc, const T* x, const T* e, const T* b, T* xo,
+                            const Terms<T>& M, int shape, T sA, T sM, T omega, cudaStream_t s);
 bool sweep_norm_supported();
 // K4 through the marching kernels: ||b - A x|| appended to the device history
 template <class T>

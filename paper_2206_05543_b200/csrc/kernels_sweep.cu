@@ -124,10 +124,16 @@ template <class T>
 __host__ __device__ constexpr int m2_width() { return 32 * m2_vec<T>() * M2_NW; }
 template <class T>
 __host__ __device__ constexpr int m2_rowlen() { return m2_width<T>() + 2 * m2_vec<T>(); }
+// NM == 3 (prolongation + correction fused in front of the sweep): coarse correction rows
+// [c0/2 - VEC, c0/2 + W/2 + VEC) staged in a ring indexed by coarse row
+constexpr int M2_CR = 8;
 template <class T>
-constexpr size_t m2_smem_bytes() {
+__host__ __device__ constexpr int m2_crowlen() { return m2_width<T>() / 2 + 2 * m2_vec<T>(); }
+template <class T>
+constexpr size_t m2_smem_bytes(bool pc = false) {
     return (size_t)2 * M2_ST * m2_rowlen<T>() * sizeof(T)   // x and b stages
            + (size_t)2 * m2_rowlen<T>() * sizeof(T)         // r rows (ring of 2)
+           + (pc ? (size_t)M2_CR * m2_crowlen<T>() * sizeof(T) : 0)  // coarse correction rows
            + (size_t)M2_ST * 8;                             // mbarriers
 }
 
@@ -153,16 +159,80 @@ struct M2Ctx {
     long long px;
     int n, c0, col, sidx, q0, q_last, r0, r_end, lane;
     bool producer, last_strip;
+    // NM == 3: coarse correction e (multigrid.py:184) staged per coarse row
+    T* es;            // ring of M2_CR coarse rows
+    const T* erow0;   // coarse row 0 at coarse column c0/2 - VEC
+    long long epx;
+    int m, ce0;       // coarse interior size, first staged coarse column
 };
 
-template <class T, int S, bool FZ>
+__device__ __forceinline__ int fl2(int q) { return q >= 0 ? q / 2 : -((1 - q) / 2); }  // floor(q/2)
+
+// x(q, .) += (P e)(q, .) on VEC staged columns starting at the even fine column k0 (staged
+// index si): separable d-linear interpolation, axis 0 first, with the reference end formulas
+// (multigrid.py:122-144) -- the k_prolong_correct2d tree.  Outside the interior P e is exactly
+// 0 (zero frame), so halo columns/rows stay 0.
+template <class T>
+__device__ __forceinline__ void m2_correct(const M2Ctx<T>& c, T* xrow, int q, int k0, int si) {
+    constexpr int VEC = m2_vec<T>();
+    constexpr int CRW = m2_crowlen<T>();
+    using O = Op<T>;
+    auto row = [&](int cr) { return c.es + ((cr % M2_CR + M2_CR) % M2_CR) * CRW - c.ce0; };
+    // axis 0: t(J) at coarse columns J0-1 .. J0+VEC/2-1 (J0 = k0/2)
+    const int J0 = k0 >> 1;
+    T t[VEC / 2 + 1];
+    if (q & 1) {
+        const T* e0 = row((q - 1) >> 1);
+#pragma unroll
+        for (int i = 0; i <= VEC / 2; ++i) t[i] = e0[J0 - 1 + i];
+    } else {
+        const int I = q >> 1;
+        const T* em = row(I - 1);
+        const T* e0 = row(I);
+#pragma unroll
+        for (int i = 0; i <= VEC / 2; ++i) t[i] = pl_even<T>(em[J0 - 1 + i], e0[J0 - 1 + i], I == 0, I == c.m);
+    }
+    // axis 1: even column 2J -> pl_even(t(J-1), t(J)), odd column 2J+1 -> t(J)
+#pragma unroll
+    for (int i = 0; i < VEC / 2; ++i) {
+        const int J = J0 + i;
+        xrow[si + 2 * i] = O::add(xrow[si + 2 * i], pl_even<T>(t[i], t[i + 1], J == 0, J == c.m));
+        xrow[si + 2 * i + 1] = O::add(xrow[si + 2 * i + 1], t[i + 1]);
+    }
+}
+
+// consumers correct the whole staged x row q (own columns; threads 0/1 also the strip halos)
+template <class T>
+__device__ __forceinline__ void m2_correct_row(const M2Ctx<T>& c, int q, int slot) {
+    constexpr int VEC = m2_vec<T>();
+    constexpr int W = m2_width<T>();
+    constexpr int RW = m2_rowlen<T>();
+    T* xrow = c.xs + slot * RW;
+    m2_correct<T>(c, xrow, q, c.col, c.sidx);
+    const int t = c.sidx / VEC - 1;  // consumer thread index 0..(W/VEC - 1)
+    if (t == 0) m2_correct<T>(c, xrow, q, c.c0 - VEC, 0);
+    if (t == 1) m2_correct<T>(c, xrow, q, c.c0 + W, VEC + W);
+}
+
+template <class T, int S, bool FZ, int NM = 0>
 __device__ __forceinline__ void m2_issue(const M2Ctx<T>& c, int q, int slot) {
     constexpr int RW = m2_rowlen<T>();
     constexpr uint32_t row_bytes = RW * sizeof(T);
+    constexpr uint32_t crow_bytes = m2_crowlen<T>() * sizeof(T);
+    // NM == 3: fine row q brings the coarse row floor(q/2) it is the first to need (the first
+    // staged row also brings the row below)
+    const int ncr = NM == 3 ? ((q & 1) == 0 || q == c.q0 ? 1 : 0) + (q == c.q0 && (q & 1) == 0 ? 1 : 0) : 0;
     fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&c.full[slot], FZ ? row_bytes : 2 * row_bytes);
+    mbar_arrive_expect_tx(&c.full[slot], (FZ ? row_bytes : 2 * row_bytes) + ncr * crow_bytes);
     if (!FZ) bulk_g2s(c.xs + slot * RW, c.xrow0 + (long long)q * c.px, row_bytes, &c.full[slot]);
     bulk_g2s(c.bs + slot * RW, c.brow0 + (long long)q * c.px, row_bytes, &c.full[slot]);
+    if constexpr (NM == 3) {
+        for (int i = 0; i < ncr; ++i) {
+            const int cr = fl2(q) - i;
+            bulk_g2s(c.es + ((cr % M2_CR + M2_CR) % M2_CR) * m2_crowlen<T>(), c.erow0 + (long long)cr * c.epx,
+                     crow_bytes, &c.full[slot]);
+        }
+    }
 }
 
 // One marching step k (row j = q0 + k): r(j) for the strip (+ halo), then output row j-1.
@@ -205,7 +275,7 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
             for (int v = 0; v < VEC; ++v)
                 if (!row_in || c.col + v >= c.n) R[ic][v] = T(0);  // r is zero outside the interior
         }
-        if (NM && j >= c.r0 && j < c.r_end) {
+        if ((NM == 1 || NM == 2) && j >= c.r0 && j < c.r_end) {
 #pragma unroll
             for (int v = 0; v < VEC; ++v) nacc += (double)R[ic][v] * (double)R[ic][v];  // ||r||^2, own rows
         }
@@ -227,10 +297,18 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
     named_bar_sync(1, (M2_NW + 1) * 32);
     if (c.producer) {
         // stage j-1 was last read before this barrier: refill its slot with row j-1+ST
-        if (c.lane == 0 && j - 1 + ST <= c.q_last) m2_issue<T, S, FZ>(c, j - 1 + ST, sm);
+        if (c.lane == 0 && j - 1 + ST <= c.q_last) m2_issue<T, S, FZ, NM>(c, j - 1 + ST, sm);
         return;
     }
     if (NM == 2) return;
+    if constexpr (NM == 3) {
+        // x + P e of row j+3 (read from step k+2 on, i.e. after the next barrier)
+        constexpr int s3 = (P + 3) % ST;
+        if (j + 3 <= c.q_last) {
+            mbar_wait(&c.full[s3], (uint32_t)(((k + 3) / ST) & 1));
+            m2_correct_row<T>(c, j + 3, s3);
+        }
+    }
     RL[ic] = rrow[c.sidx - 1];
     RH[ic] = rrow[c.sidx + VEC];
     if (j - 1 < c.r0) return;
@@ -263,7 +341,7 @@ template <class T, int S, bool FZ, int NM>
 __global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, const T* __restrict__ x,
                                                                      const T* __restrict__ b, T* __restrict__ xo,
                                                                      Terms<T> M, T sA, T sM, T omega, int rows,
-                                                                     NormOut no) {
+                                                                     NormOut no, const T* __restrict__ e, Layout Lc) {
     constexpr int VEC = m2_vec<T>();
     constexpr int W = m2_width<T>();
     constexpr int RW = m2_rowlen<T>();
@@ -275,7 +353,8 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, co
     c.xs = reinterpret_cast<T*>(smem_raw);
     c.bs = c.xs + ST * RW;
     c.rr = c.bs + ST * RW;
-    c.full = reinterpret_cast<uint64_t*>(c.rr + 2 * RW);
+    c.es = c.rr + 2 * RW;
+    c.full = reinterpret_cast<uint64_t*>(c.es + (NM == 3 ? M2_CR * m2_crowlen<T>() : 0));
     const int warp = threadIdx.x >> 5;
     c.lane = threadIdx.x & 31;
     c.producer = warp == M2_NW;
@@ -293,6 +372,12 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, co
     c.xrow0 = x + L.origin + (c.c0 - VEC);
     c.brow0 = b + L.origin + (c.c0 - VEC);
     c.orow0 = xo + L.origin + c.col;
+    if constexpr (NM == 3) {
+        c.ce0 = c.c0 / 2 - VEC;
+        c.erow0 = e + Lc.origin + c.ce0;
+        c.epx = Lc.px;
+        c.m = Lc.n;
+    }
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < ST; ++i) mbar_init(&c.full[i], 1);
@@ -300,7 +385,7 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, co
     }
     __syncthreads();
     if (c.producer && c.lane == 0)
-        for (int q = c.q0; q < c.q0 + ST && q <= c.q_last; ++q) m2_issue<T, S, FZ>(c, q, q - c.q0);
+        for (int q = c.q0; q < c.q0 + ST && q <= c.q_last; ++q) m2_issue<T, S, FZ, NM>(c, q, q - c.q0);
 
     T X[3][VEC], R[3][VEC], RL[3], RH[3];
 #pragma unroll
@@ -311,6 +396,14 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, co
     }
     mbar_wait(&c.full[0], 0);
     mbar_wait(&c.full[1], 0);
+    if constexpr (NM == 3) {  // rows q0 .. q0+3 corrected before the march (then 2 steps ahead)
+        if (!c.producer)
+            for (int i = 0; i < 4 && c.q0 + i <= c.q_last; ++i) {
+                mbar_wait(&c.full[i], 0);
+                m2_correct_row<T>(c, c.q0 + i, i);
+            }
+        __syncthreads();
+    }
     if (!FZ && !c.producer) {
         V16<T>::ld(c.xs + 0 * RW + c.sidx, X[0]);  // x(q0)   = x(j-1) of step k = 1
         V16<T>::ld(c.xs + 1 * RW + c.sidx, X[1]);  // x(q0+1) = x(j)
@@ -325,13 +418,21 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, co
         if (kb + 4 <= K) m2_step<T, S, FZ, NM, 4>(c, kb + 4, X, R, RL, RH, M, sA, sM, omega, nacc);
         if (kb + 5 <= K) m2_step<T, S, FZ, NM, 5>(c, kb + 5, X, R, RL, RH, M, sA, sM, omega, nacc);
     }
-    if (NM) norm_epilogue(nacc, no);
+    if (NM == 1 || NM == 2) norm_epilogue(nacc, no);
 }
 
 template <class T, int S, bool FZ, int NM>
 static cudaError_t launch_sweep2d_march(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA,
-                                        T sM, T omega, const NormOut& no, cudaStream_t s) {
-    constexpr size_t smem = m2_smem_bytes<T>();
+                                        T sM, T omega, const NormOut& no, cudaStream_t s, const T* e = nullptr,
+                                        const Layout* Lc = nullptr) {
+    constexpr size_t smem = m2_smem_bytes<T>(NM == 3);
+    static bool attr = false;
+    if (!attr && smem > 48 * 1024) {
+        cudaError_t err = cudaFuncSetAttribute(k_sweep2d_march<T, S, FZ, NM>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (err != cudaSuccess) return err;
+        attr = true;
+    }
     constexpr int threads = (M2_NW + 1) * 32;
     static int occ = 0;
     if (!occ) {
@@ -347,7 +448,7 @@ static cudaError_t launch_sweep2d_march(const Layout& L, const T* x, const T* b,
     chunks = (L.n + rows - 1) / rows;
     dim3 g(strips, chunks);
     return launch_pdl(k_sweep2d_march<T, S, FZ, NM>, g, dim3(threads), smem, s, L, x, b, xo, M, sA, sM, omega, rows,
-                      no);
+                      no, e, Lc ? *Lc : L);
 }
 
 bool sweep_fused_supported(int dim, int shape) {
@@ -411,6 +512,28 @@ cudaError_t launch_sweep(const Layout& L, const T* x, const T* b, T* xo, const T
     return sweep_fz<T, SHAPE_GENERIC>(L, x, b, xo, M, sA, sM, omega, from_zero, no, s);
 }
 
+// K3 + K1 fused: xo = sweep(x + P e) for the first post-smoothing step (multigrid.py:184-185);
+// 2D marching levels only (the prolongation is applied to every staged x value on the fly)
+bool sweep_pc_supported(const Layout& L) {
+    const char* e = getenv("SPAIMG_PC");
+    return L.dim == 2 && L.N > flat_threshold(2) && !sweep_v1() && !(e && e[0] == '0');
+}
+
+template <class T>
+cudaError_t launch_sweep_pc(const Layout& L, const Layout& Lc, const T* x, const T* e, const T* b, T* xo,
+                            const Terms<T>& M, int shape, T sA, T sM, T omega, cudaStream_t s) {
+    const NormOut none{};
+    switch (shape) {
+        case SHAPE_C1: return launch_sweep2d_march<T, SHAPE_C1, false, 3>(L, x, b, xo, M, sA, sM, omega, none, s, e, &Lc);
+        case SHAPE_STAR5:
+            return launch_sweep2d_march<T, SHAPE_STAR5, false, 3>(L, x, b, xo, M, sA, sM, omega, none, s, e, &Lc);
+        case SHAPE_BOX9:
+            return launch_sweep2d_march<T, SHAPE_BOX9, false, 3>(L, x, b, xo, M, sA, sM, omega, none, s, e, &Lc);
+        default:
+            return launch_sweep2d_march<T, SHAPE_GENERIC, false, 3>(L, x, b, xo, M, sA, sM, omega, none, s, e, &Lc);
+    }
+}
+
 // residual norm alone through the marching machinery (no smoothing output)
 template <class T>
 cudaError_t launch_norm_march(const Layout& L, const T* x, const T* b, T sA, const NormOut& no, cudaStream_t s) {
@@ -446,6 +569,11 @@ template cudaError_t launch_sweep<double>(const Layout&, const double*, const do
                                           int, double, double, double, bool, cudaStream_t, const NormOut*);
 template cudaError_t launch_sweep<float>(const Layout&, const float*, const float*, float*, const Terms<float>&, int,
                                          float, float, float, bool, cudaStream_t, const NormOut*);
+template cudaError_t launch_sweep_pc<double>(const Layout&, const Layout&, const double*, const double*,
+                                             const double*, double*, const Terms<double>&, int, double, double, double,
+                                             cudaStream_t);
+template cudaError_t launch_sweep_pc<float>(const Layout&, const Layout&, const float*, const float*, const float*,
+                                            float*, const Terms<float>&, int, float, float, float, cudaStream_t);
 template cudaError_t launch_norm_march<double>(const Layout&, const double*, const double*, double, const NormOut&,
                                                cudaStream_t);
 template cudaError_t launch_norm_march<float>(const Layout&, const float*, const float*, float, const NormOut&,

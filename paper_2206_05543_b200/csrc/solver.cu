@@ -744,6 +744,19 @@ template <class T> struct Solver final : spaimg_solver {
             if (c < 0) return -1;
         }
         const int ao = (l == 0 && k3_flip) ? 1 - a : a;
+        if (cfg.nu2 >= 1 && fused && ao == a && sweep_pc_supported(L.L)) {
+            // prolongation + correction fused into the first post-sweep: x + P e never hits HBM
+            if (launch_sweep_pc<T>(L.L, C.L, L.x[a], C.x[c], L.b, L.x[1 - a], M, shape, L.sA, L.sM, omega, s) !=
+                cudaSuccess)
+                return -1;
+            ++*launches;
+            a = 1 - a;
+            for (int k = 1; k < cfg.nu2; ++k) {
+                if (do_sweep<T>(L, a, false, M, shape, fused, omega, s, launches)) return -1;
+                a = 1 - a;
+            }
+            return a;
+        }
         if (launch_prolong_correct<T>(L.L, C.L, L.x[a], L.x[ao], C.x[c], s) != cudaSuccess) return -1;
         ++*launches;
         a = ao;
