@@ -69,6 +69,9 @@ cudaError_t launch_residual_restrict(const Layout& Lf, const Layout& Lc, const T
 // N <= flat_threshold(dim) use them instead of the marching kernels
 int flat_threshold(int dim);
 template <class T>
+cudaError_t launch_sweep_pc_flat(const Layout& L, const Layout& Lc, const T* x, const T* e, const T* b, T* xo,
+                                 const Terms<T>& M, int shape, T sA, T sM, T omega, cudaStream_t s);
+template <class T>
 cudaError_t launch_residual_restrict_flat(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T sA,
                                           cudaStream_t s);
 

@@ -126,7 +126,9 @@ template <class T>
 __host__ __device__ constexpr int m2_rowlen() { return m2_width<T>() + 2 * m2_vec<T>(); }
 // NM == 3 (prolongation + correction fused in front of the sweep): coarse correction rows
 // [c0/2 - VEC, c0/2 + W/2 + VEC) staged in a ring indexed by coarse row
-constexpr int M2_CR = 8;
+// ring depth: at step j the consumers read coarse rows fl2(j+3)-1 .. fl2(j+3) while the producer
+// stages fl2(j+5), so 4 slots never alias a live row
+constexpr int M2_CR = 4;
 template <class T>
 __host__ __device__ constexpr int m2_crowlen() { return m2_width<T>() / 2 + 2 * m2_vec<T>(); }
 template <class T>
@@ -514,14 +516,26 @@ cudaError_t launch_sweep(const Layout& L, const T* x, const T* b, T* xo, const T
 
 // K3 + K1 fused: xo = sweep(x + P e) for the first post-smoothing step (multigrid.py:184-185);
 // 2D marching levels only (the prolongation is applied to every staged x value on the fly)
+// 2D marching levels: the marching kernel with the correction applied to every staged x row
+// (NM == 3); flat levels (opt-in, SPAIMG_PC_FLAT=1): k_sweep{2,3}d_tile_pc (kernels_flat.cu).
+// Measured (tools/tune.py): the marching fusion is a net win on the 4096^2 level (-16 B/unknown
+// of HBM traffic) and a loss on 2048^2 (its extra per-step work is not hidden once the level's
+// HBM time is short); the flat fusion is neutral in 2D and a loss in 3D (small levels are bound
+// by the latency of their dependent loads, which the fusion lengthens).
 bool sweep_pc_supported(const Layout& L) {
     const char* e = getenv("SPAIMG_PC");
-    return L.dim == 2 && L.N > flat_threshold(2) && !sweep_v1() && !(e && e[0] == '0');
+    if (sweep_v1() || (e && e[0] == '0')) return false;
+    if (L.N <= flat_threshold(L.dim)) {
+        const char* f = getenv("SPAIMG_PC_FLAT");
+        return f && f[0] == '1';
+    }
+    return L.dim == 2 && L.N > 2048;
 }
 
 template <class T>
 cudaError_t launch_sweep_pc(const Layout& L, const Layout& Lc, const T* x, const T* e, const T* b, T* xo,
                             const Terms<T>& M, int shape, T sA, T sM, T omega, cudaStream_t s) {
+    if (L.N <= flat_threshold(L.dim)) return launch_sweep_pc_flat<T>(L, Lc, x, e, b, xo, M, shape, sA, sM, omega, s);
     const NormOut none{};
     switch (shape) {
         case SHAPE_C1: return launch_sweep2d_march<T, SHAPE_C1, false, 3>(L, x, b, xo, M, sA, sM, omega, none, s, e, &Lc);
