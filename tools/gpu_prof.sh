@@ -1,13 +1,25 @@
 #!/bin/bash
-# ncu campaign (one GPU): eager launch list of one bench solve + --set full captures of each hot kernel.
+# ncu campaign (one GPU): bench line, eager launch lists of one solve (c2, c4), --set full of each hot kernel.
 mkdir -p gpurun_out
 NCU="ncu --set full --clock-control none --import-source on -f"
-SPAIMG_NO_GRAPH=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
-  --log-file gpurun_out/launches_c2.csv python tools/prof_op.py c2 9 1 > gpurun_out/ncu_l2.log 2>&1; echo l2=$?
-SPAIMG_NO_GRAPH=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
-  --log-file gpurun_out/launches_c4.csv python tools/prof_op.py c4 9 1 > gpurun_out/ncu_l4.log 2>&1; echo l4=$?
-for spec in "c2 0 sweep2d" "c2 1 residual_restrict2d" "c2 2 prolong" "c2 3 norm" "c4 0 sweep3d" "c4 1 ." "c4 2 prolong" "c4 3 ."; do
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench=$?
+for c in c2 c4; do
+  SPAIMG_NO_GRAPH=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
+    --log-file gpurun_out/launches_$c.csv python tools/prof_op.py $c 9 1 > gpurun_out/ncu_l_$c.log 2>&1; echo launches_$c=$?
+done
+for spec in "c2 0 sweep2d" "c2 1 residual_restrict2d" "c2 2 prolong" "c4 0 sweep3d" "c4 1 sweep3d" "c4 2 prolong"; do
   set -- $spec
-  timeout 600 $NCU -k regex:$3 -s 2 -c 2 -o gpurun_out/full_$1_op$2 python tools/prof_op.py $1 $2 4 > gpurun_out/ncu_full_$1_$2.log 2>&1
+  timeout 600 $NCU -k regex:$3 -s 2 -c 1 -o gpurun_out/full_$1_op$2 python tools/prof_op.py $1 $2 4 > gpurun_out/ncu_full_$1_$2.log 2>&1
   echo full_$1_$2=$?
 done
+SPAIMG_NO_GRAPH=1 timeout 600 $NCU --kernel-name-base demangled -k "regex:\(int\)3, \(bool\)0, \(int\)3" -s 1 -c 1 \
+  -o gpurun_out/full_c2_pc python tools/prof_op.py c2 9 2 > gpurun_out/ncu_full_pc.log 2>&1; echo full_pc=$?
+timeout 600 $NCU -k regex:k_tail -s 2 -c 1 -o gpurun_out/full_c2_tail python tools/prof_op.py c2 9 3 > gpurun_out/ncu_full_tail.log 2>&1; echo full_tail=$?
+# keep the merge-back small: export the reports to CSV on the box, drop the .ncu-rep files
+for r in gpurun_out/full_*.ncu-rep; do
+  b=${r%.ncu-rep}
+  ncu -i $r --page raw --csv > $b.raw.csv 2>/dev/null
+  ncu -i $r --page details --csv > $b.details.csv 2>/dev/null
+  rm -f $r
+done
+du -sh gpurun_out

@@ -44,7 +44,11 @@ def _num(v):
 
 
 def raw_rows(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+    if rep.endswith(".csv"):  # `ncu -i <rep> --page raw --csv` exported on the GPU box
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
+                             check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     res = []
@@ -86,7 +90,7 @@ def full(reps, out, traffic):
                 tot = si(d, "dram__bytes_read.sum") + si(d, "dram__bytes_write.sum")
                 lines.append(f"| DRAM bytes per launch (rd+wr) | {tot:.4g} B |")
                 for key, r2 in traffic:
-                    if os.path.samefile(r2, rep):
+                    if os.path.abspath(r2) == os.path.abspath(rep):
                         tr[key] = tot
             lines.append("")
     with open(out, "w") as f:
