@@ -128,7 +128,7 @@ __host__ __device__ constexpr int m2_rowlen() { return m2_width<T>() + 2 * m2_ve
 // [c0/2 - VEC, c0/2 + W/2 + VEC) staged in a ring indexed by coarse row
 // ring depth: at step j the consumers read coarse rows fl2(j+3)-1 .. fl2(j+3) while the producer
 // stages fl2(j+5), so 4 slots never alias a live row
-constexpr int M2_CR = 4;
+constexpr int M2_CR = 4;  // must be a power of 2
 template <class T>
 __host__ __device__ constexpr int m2_crowlen() { return m2_width<T>() / 2 + 2 * m2_vec<T>(); }
 template <class T>
@@ -179,7 +179,7 @@ __device__ __forceinline__ void m2_correct(const M2Ctx<T>& c, T* xrow, int q, in
     constexpr int VEC = m2_vec<T>();
     constexpr int CRW = m2_crowlen<T>();
     using O = Op<T>;
-    auto row = [&](int cr) { return c.es + ((cr % M2_CR + M2_CR) % M2_CR) * CRW - c.ce0; };
+    auto row = [&](int cr) { return c.es + (cr & (M2_CR - 1)) * CRW - c.ce0; };  // M2_CR: power of 2
     // axis 0: t(J) at coarse columns J0-1 .. J0+VEC/2-1 (J0 = k0/2)
     const int J0 = k0 >> 1;
     T t[VEC / 2 + 1];
@@ -195,12 +195,15 @@ __device__ __forceinline__ void m2_correct(const M2Ctx<T>& c, T* xrow, int q, in
         for (int i = 0; i <= VEC / 2; ++i) t[i] = pl_even<T>(em[J0 - 1 + i], e0[J0 - 1 + i], I == 0, I == c.m);
     }
     // axis 1: even column 2J -> pl_even(t(J-1), t(J)), odd column 2J+1 -> t(J)
+    T xv[VEC];
+    V16<T>::ld(xrow + si, xv);
 #pragma unroll
     for (int i = 0; i < VEC / 2; ++i) {
         const int J = J0 + i;
-        xrow[si + 2 * i] = O::add(xrow[si + 2 * i], pl_even<T>(t[i], t[i + 1], J == 0, J == c.m));
-        xrow[si + 2 * i + 1] = O::add(xrow[si + 2 * i + 1], t[i + 1]);
+        xv[2 * i] = O::add(xv[2 * i], pl_even<T>(t[i], t[i + 1], J == 0, J == c.m));
+        xv[2 * i + 1] = O::add(xv[2 * i + 1], t[i + 1]);
     }
+    V16<T>::st(xrow + si, xv);
 }
 
 // consumers correct the whole staged x row q (own columns; threads 0/1 also the strip halos)
@@ -211,9 +214,10 @@ __device__ __forceinline__ void m2_correct_row(const M2Ctx<T>& c, int q, int slo
     constexpr int RW = m2_rowlen<T>();
     T* xrow = c.xs + slot * RW;
     m2_correct<T>(c, xrow, q, c.col, c.sidx);
+    // the strip halos go to the first and the last consumer (different warps)
     const int t = c.sidx / VEC - 1;  // consumer thread index 0..(W/VEC - 1)
     if (t == 0) m2_correct<T>(c, xrow, q, c.c0 - VEC, 0);
-    if (t == 1) m2_correct<T>(c, xrow, q, c.c0 + W, VEC + W);
+    if (t == W / VEC - 1) m2_correct<T>(c, xrow, q, c.c0 + W, VEC + W);
 }
 
 template <class T, int S, bool FZ, int NM = 0>
