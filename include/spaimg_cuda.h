@@ -136,6 +136,14 @@ SPAIMG_API int spaimg_solver_run(spaimg_solver *s, double tol, int max_iters, do
                       int *converged, void *stream);
 /* copy the current finest iterate out (dense layout) */
 SPAIMG_API int spaimg_solver_store(spaimg_solver *s, void *u_out, void *stream);
+/* nrhs independent zero-start solves of the solver's problem (solve() loop of multigrid.py:206-219
+ * per right-hand side), pipelined: b[i+1] is copied in and u_out[i-1] copied out on their own
+ * streams while solve i runs.  b[i] / u_out[i]: dense (N-1)^dim arrays, host (pinned for the
+ * overlap) or device.  norms: nrhs x (max_iters+1) row-major (row i holds ||r_0|| .. ||r_k||);
+ * iterations / converged: nrhs each.  Returns when every output has landed. */
+SPAIMG_API int spaimg_solver_solve_batch(spaimg_solver *s, int nrhs, const void *const *b, void *const *u_out,
+                                         double tol, int max_iters, double *norms, int *iterations, int *converged,
+                                         void *stream);
 
 /* Isolated kernel launches on the solver's finest-level buffers, for per-operator timing
  * (BASELINE.json config 5): op 0 = fused sweep (K1), 1 = residual+restriction (K2),

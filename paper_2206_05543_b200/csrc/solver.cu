@@ -386,6 +386,8 @@ struct spaimg_solver {
     virtual int cycles(int n, cudaStream_t s) = 0;
     virtual int run(double tol, int max_iters, double* norms, int* iters, int* conv, cudaStream_t s) = 0;
     virtual int store(void* out, cudaStream_t s) = 0;
+    virtual int solve_batch(int nrhs, const void* const* b, void* const* u, double tol, int max_iters, double* norms,
+                            int* iters, int* conv, cudaStream_t s) = 0;
     virtual int op(int which, int reps, cudaStream_t s) = 0;
     virtual void stats(spaimg_solver_stats* st) const = 0;
 };
@@ -465,6 +467,20 @@ template <class T> struct Solver final : spaimg_solver {
     size_t tail_arr_off = 0, tail_smem = 0;
 
     ~Solver() override {
+        if (bs_h2d) {
+            cudaStreamSynchronize(bs_h2d);
+            cudaStreamSynchronize(bs_d2h);
+            cudaStreamDestroy(bs_h2d);
+            cudaStreamDestroy(bs_d2h);
+            for (int i = 0; i < 2; ++i) {
+                cudaEventDestroy(ev_in[i]);
+                cudaEventDestroy(ev_pad[i]);
+                cudaEventDestroy(ev_unpad[i]);
+                cudaEventDestroy(ev_out[i]);
+            }
+            cudaEventDestroy(ev_go);
+        }
+        if (bnorms_h) cudaFreeHost(bnorms_h);
         if (exec_cycle) cudaGraphExecDestroy(exec_cycle);
         if (exec_solve) cudaGraphExecDestroy(exec_solve);
         for (auto& kv : op_graphs) cudaGraphExecDestroy(kv.second);
@@ -954,6 +970,96 @@ template <class T> struct Solver final : spaimg_solver {
         return store_dense<T>(sc, lv[0].L, lv[0].x[0], out, s, stage);
     }
 
+    // ---- pipelined independent solves (host in -> device solve -> host out) -----------------
+    // Right-hand side i+1 is copied in (own stream) and solution i-1 copied out (own stream)
+    // while solve i runs, through two dense device staging buffers per direction; with pinned
+    // host buffers PCIe traffic in both directions overlaps the solves.
+    cudaStream_t bs_h2d = nullptr, bs_d2h = nullptr;
+    cudaEvent_t ev_in[2] = {}, ev_pad[2] = {}, ev_unpad[2] = {}, ev_out[2] = {}, ev_go = nullptr;
+    T* bstage_in[2] = {};
+    T* bstage_out[2] = {};
+    double* bnorms_h = nullptr;  // pinned: per solve max_iters+1 norms + 2 state ints (as doubles)
+    int bnorms_cap = 0;
+
+    int batch_init(int per_solve, int nrhs) {
+        if (!bs_h2d) {
+            CK(cudaStreamCreateWithFlags(&bs_h2d, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&bs_d2h, cudaStreamNonBlocking));
+            for (int i = 0; i < 2; ++i) {
+                CK(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&ev_pad[i], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&ev_unpad[i], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming));
+                const size_t cnt = (size_t)count_of(cfg.dim, cfg.N);
+                if (int rc = dalloc(&bstage_in[i], cnt)) return rc;
+                if (int rc = dalloc(&bstage_out[i], cnt)) return rc;
+            }
+            CK(cudaEventCreateWithFlags(&ev_go, cudaEventDisableTiming));
+        }
+        if (per_solve * nrhs > bnorms_cap) {
+            if (bnorms_h) cudaFreeHost(bnorms_h);
+            bnorms_h = nullptr;
+            CK(cudaMallocHost(&bnorms_h, sizeof(double) * per_solve * nrhs));
+            bnorms_cap = per_solve * nrhs;
+        }
+        return 0;
+    }
+
+    int solve_batch(int nrhs, const void* const* bh, void* const* uh, double tol, int max_iters, double* norms,
+                    int* iters, int* conv, cudaStream_t s) override {
+        if (max_iters + 1 > norms_cap) return fail(SPAIMG_EINVAL, "max_iters too large");
+        if (nrhs <= 0) return 0;
+        if (!use_graph) return fail(SPAIMG_ENOTSUP, "solve_batch needs the graph path");
+        if (!exec_solve)
+            if (int rc = build_solve_graph()) return rc;
+        const int per = max_iters + 1 + 2;
+        if (int rc = batch_init(per, nrhs)) return rc;
+        const size_t bytes = (size_t)count_of(cfg.dim, cfg.N) * sizeof(T);
+        Level<T>& L0 = lv[0];
+        ctl_h->tol = tol;
+        ctl_h->max_iters = max_iters;
+        CK(cudaMemcpyAsync(ctl_d, ctl_h, sizeof(SolveCtl), cudaMemcpyHostToDevice, s));
+        CK(cudaEventRecord(ev_go, s));
+        CK(cudaStreamWaitEvent(bs_h2d, ev_go, 0));
+        CK(cudaStreamWaitEvent(bs_d2h, ev_go, 0));
+        CK(cudaMemcpyAsync(bstage_in[0], bh[0], bytes, cudaMemcpyHostToDevice, bs_h2d));
+        CK(cudaEventRecord(ev_in[0], bs_h2d));
+        for (int i = 0; i < nrhs; ++i) {
+            const int c = i & 1, o = c ^ 1;
+            if (i + 1 < nrhs) {  // prefetch the next right-hand side once its stage is free
+                if (i >= 1) CK(cudaStreamWaitEvent(bs_h2d, ev_pad[o], 0));
+                CK(cudaMemcpyAsync(bstage_in[o], bh[i + 1], bytes, cudaMemcpyHostToDevice, bs_h2d));
+                CK(cudaEventRecord(ev_in[o], bs_h2d));
+            }
+            CK(cudaStreamWaitEvent(s, ev_in[c], 0));
+            CK(launch_pad<T>(L0.L, bstage_in[c], L0.b, s));
+            CK(cudaEventRecord(ev_pad[c], s));
+            CK(cudaMemsetAsync(L0.x[0], 0, (size_t)L0.L.alloc * sizeof(T), s));
+            CK(cudaGraphLaunch(exec_solve, s));
+            CK(cudaMemcpyAsync(bnorms_h + (size_t)i * per, norms_d, sizeof(double) * (max_iters + 1),
+                               cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(bnorms_h + (size_t)i * per + max_iters + 1, state_d, 2 * sizeof(int),
+                               cudaMemcpyDeviceToHost, s));
+            if (i >= 2) CK(cudaStreamWaitEvent(s, ev_out[c], 0));  // solution i-2 left this stage
+            CK(launch_unpad<T>(L0.L, L0.x[0], bstage_out[c], s));
+            CK(cudaEventRecord(ev_unpad[c], s));
+            CK(cudaStreamWaitEvent(bs_d2h, ev_unpad[c], 0));
+            CK(cudaMemcpyAsync(uh[i], bstage_out[c], bytes, cudaMemcpyDeviceToHost, bs_d2h));
+            CK(cudaEventRecord(ev_out[c], bs_d2h));
+        }
+        CK(cudaStreamWaitEvent(s, ev_out[(nrhs - 1) & 1], 0));
+        CK(cudaStreamSynchronize(s));
+        for (int i = 0; i < nrhs; ++i) {
+            const double* h = bnorms_h + (size_t)i * per;
+            int st[2];
+            std::memcpy(st, h + max_iters + 1, sizeof(st));
+            iters[i] = st[0];
+            conv[i] = st[1];
+            for (int k = 0; k <= st[0]; ++k) norms[(size_t)i * (max_iters + 1) + k] = h[k];
+        }
+        return 0;
+    }
+
     int op_launch(int which, cudaStream_t s) {
         Level<T>& L = lv[0];
         if (nsmooth() < 1) return fail(SPAIMG_EINVAL, "no smoothing level");
@@ -1081,6 +1187,17 @@ extern "C" int spaimg_solver_run(spaimg_solver* s, double tol, int max_iters, do
     if (!s || !norms || !iterations || !converged) return fail(SPAIMG_EINVAL, "NULL argument");
     if (max_iters < 0) return fail(SPAIMG_EINVAL, "max_iters must be non-negative");
     return s->run(tol, max_iters, norms, iterations, converged, (cudaStream_t)stream);
+}
+
+extern "C" int spaimg_solver_solve_batch(spaimg_solver* s, int nrhs, const void* const* b, void* const* u_out,
+                                         double tol, int max_iters, double* norms, int* iterations, int* converged,
+                                         void* stream) {
+    if (!s || (nrhs > 0 && (!b || !u_out || !norms || !iterations || !converged)))
+        return fail(SPAIMG_EINVAL, "NULL argument");
+    if (nrhs < 0 || max_iters < 0) return fail(SPAIMG_EINVAL, "nrhs and max_iters must be non-negative");
+    for (int i = 0; i < nrhs; ++i)
+        if (!b[i] || !u_out[i]) return fail(SPAIMG_EINVAL, "NULL right-hand side or output");
+    return s->solve_batch(nrhs, b, u_out, tol, max_iters, norms, iterations, converged, (cudaStream_t)stream);
 }
 
 extern "C" int spaimg_solver_store(spaimg_solver* s, void* u_out, void* stream) {

@@ -465,6 +465,30 @@ class Solver:
         k = iters.value
         return [float(norms[i]) for i in range(k + 1)], k, bool(conv.value)
 
+    def solve_batch(self, b_list, u_list, tol=None, max_iters=None, stream=None):
+        """Independent zero-start solves of each b in `b_list` into the matching `u_list` array,
+        pipelined so that host<->device copies overlap the solves (pass pinned host tensors or
+        device tensors).  Returns [(residual_norms, iterations, converged), ...]."""
+        if len(b_list) != len(u_list):
+            raise ValueError("b_list and u_list must have the same length")
+        tol = self.cfg.tol if tol is None else tol
+        max_iters = self.cfg.max_iters if max_iters is None else max_iters
+        n = len(b_list)
+        keep = [self._ptr(v)[0] for v in list(b_list) + list(u_list)]
+        bp = (ctypes.c_void_p * n)(*[k.ptr for k in keep[:n]])
+        up = (ctypes.c_void_p * n)(*[k.ptr for k in keep[n:]])
+        norms = (ctypes.c_double * (n * (max_iters + 1)))()
+        iters = (ctypes.c_int * n)()
+        conv = (ctypes.c_int * n)()
+        _lib.check(self.lib.spaimg_solver_solve_batch(self.handle, n, bp, up, float(tol), int(max_iters), norms, iters,
+                                                      conv, self._stream(stream)))
+        out = []
+        for i in range(n):
+            k = iters[i]
+            out.append(([float(norms[i * (max_iters + 1) + j]) for j in range(k + 1)], k, bool(conv[i])))
+        del keep
+        return out
+
     def store(self, out_values, stream=None):
         ok, op = self._ptr(out_values)
         _lib.check(self.lib.spaimg_solver_store(self.handle, op, self._stream(stream)))
