@@ -157,7 +157,12 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
 #pragma unroll
                 for (int v = 0; v < VEC; ++v) up[v] = X[ic][0][v];
             }
-            const T left = xrow[-1], right = xrow[VEC];
+            // horizontal neighbours from the adjacent lanes (a warp spans a whole tile row); only
+            // the tile-edge lanes read the staged halo columns
+            T left = __shfl_up_sync(0xffffffffu, X[ic][yy][VEC - 1], 1);
+            T right = __shfl_down_sync(0xffffffffu, X[ic][yy][0], 1);
+            if ((c.tid & 31) == 0) left = xrow[-1];
+            if ((c.tid & 31) == 31) right = xrow[VEC];
 #pragma unroll
             for (int v = 0; v < VEC; ++v) {
                 const T xe = v + 1 < VEC ? X[ic][yy][v + 1] : right;
@@ -178,10 +183,11 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
     }
     // ---- r(j) on the one-point ring of the tile, spread over all warps ------------------------
     if (NM != 2) {
-        const int lane = c.tid & 31, w = c.tid >> 5;
+        // consecutive threads take consecutive ring points, so the top/bottom ring rows are read
+        // as contiguous shared-memory runs
 #pragma unroll
         for (int base = 0; base < G::NRING; base += M3_THREADS) {
-            const int i = base + lane * M3_NW + w;
+            const int i = base + c.tid;
             if (i < G::NRING) {
                 int ry, rx;
                 if (i < G::TX) {
@@ -219,6 +225,12 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
         const int row = c.yl + yy;
         const int so = (row + 1) * RW + VEC + c.xl;  // own position in an r plane
         T out[VEC];
+        // r(j-1) one column left of the lane's first / right of its last column: adjacent lanes
+        // (the tile-edge lanes read the shared r plane)
+        T rl = __shfl_up_sync(0xffffffffu, R[im][yy][VEC - 1], 1);
+        T rr = __shfl_down_sync(0xffffffffu, R[im][yy][0], 1);
+        if ((c.tid & 31) == 0) rl = r1[so - 1];
+        if ((c.tid & 31) == 31) rr = r1[so + VEC];
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
             T acc = T(0);
@@ -242,6 +254,8 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
                     val = R[im][1 - yy][v];  // in-plane row neighbour held by this thread
                 } else if (o0 == 0 && o1 == 0 && v + o2 >= 0 && v + o2 < VEC) {
                     val = R[im][yy][v + o2];
+                } else if (o0 == 0 && o1 == 0 && (o2 == -1 || o2 == 1)) {
+                    val = o2 < 0 ? rl : rr;
                 } else {
                     const T* pl = o0 == 0 ? r1 : (o0 > 0 ? r0 : r2);
                     val = pl[so + o1 * RW + v + o2];
