@@ -60,31 +60,44 @@ struct M3Ctx {
     int cm;
 };
 
-// K2 output of coarse plane I = (j-2)/2 from the r ring planes j-2, j-1, j: full weighting
-// along axis 0, then axis 1, then axis 2 (multigrid.py:104-119), the k_restrict tree.
+// K2 output of coarse plane I = (j-2)/2 from r planes j-2, j-1, j: full weighting along axis 0,
+// then axis 1, then axis 2 (multigrid.py:104-119), the k_restrict tree.  Warp w owns coarse row
+// y0/2 + w and each lane VEC/2 coarse columns: the axis-0 weights of its own 2 x VEC fine points
+// come from the r registers, fine row 2w+2 from the shared r planes, and the column to the right
+// from the next lane (the last lane reads the shared ring column).
 template <class T>
-__device__ __forceinline__ void m3_restrict_out(const M3Ctx<T>& c, int j, const T* r0, const T* r1, const T* r2) {
+__device__ __forceinline__ void m3_restrict_out(const M3Ctx<T>& c, int j, const T* r0, const T* r1, const T* r2,
+                                                const T (&Rj)[2][M3<T>::VEC], const T (&Rj1)[2][M3<T>::VEC],
+                                                const T (&Rj2)[2][M3<T>::VEC]) {
     using G = M3<T>;
-    constexpr int CY = G::TY / 2, CX = G::TX / 2;
+    constexpr int VEC = G::VEC;
+    constexpr int RW = G::RW;
     const int I = (j - 2) >> 1;
+    const int lane = c.tid & 31;
+    T t[3][VEC + 1];
 #pragma unroll
-    for (int q0 = 0; q0 < CY * CX; q0 += M3_THREADS) {
-        const int q = q0 + c.tid;
-        const int yc = q / CX, xc = q % CX;
-        const int Y = (c.y0 >> 1) + yc, X = (c.x0 >> 1) + xc;
-        if (q >= CY * CX || Y >= c.cm || X >= c.cm) continue;
+    for (int yy = 0; yy < 2; ++yy)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) t[yy][v] = fw<T>(Rj2[yy][v], Rj1[yy][v], Rj[yy][v]);
+    const int s2 = (c.yl + 3) * RW + VEC + c.xl;  // fine row yl+2 (the next warp's / ring row)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) t[2][v] = fw<T>(r2[s2 + v], r1[s2 + v], r0[s2 + v]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        t[a][VEC] = __shfl_down_sync(0xffffffffu, t[a][0], 1);
+        if (lane == 31) {
+            const int sa = (c.yl + a + 1) * RW + VEC + c.xl + VEC;
+            t[a][VEC] = fw<T>(r2[sa], r1[sa], r0[sa]);
+        }
+    }
+    const int Y = (c.y0 >> 1) + (c.yl >> 1);
+#pragma unroll
+    for (int i = 0; i < VEC / 2; ++i) {
+        const int X = (c.x0 >> 1) + (c.xl >> 1) + i;
         T u[3];
 #pragma unroll
-        for (int qk = 0; qk < 3; ++qk) {
-            T t[3];
-#pragma unroll
-            for (int qj = 0; qj < 3; ++qj) {
-                const int so = (2 * yc + qj + 1) * G::RW + G::VEC + 2 * xc + qk;
-                t[qj] = fw<T>(r2[so], r1[so], r0[so]);
-            }
-            u[qk] = fw<T>(t[0], t[1], t[2]);
-        }
-        c.cb[c.corg + (long long)I * c.cpp + (long long)Y * c.cpx + X] = fw<T>(u[0], u[1], u[2]);
+        for (int qk = 0; qk < 3; ++qk) u[qk] = fw<T>(t[0][2 * i + qk], t[1][2 * i + qk], t[2][2 * i + qk]);
+        if (Y < c.cm && X < c.cm) c.cb[c.corg + (long long)I * c.cpp + (long long)Y * c.cpx + X] = fw<T>(u[0], u[1], u[2]);
     }
 }
 
@@ -210,7 +223,8 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
     __syncthreads();
     if (c.tid == 0 && j - 1 + M3_ST <= c.q_last) m3_issue<T, FZ>(c, xmap, bmap, j - 1 + M3_ST, sm);
     if constexpr (NM == 3) {
-        if ((j & 1) == 0 && j >= c.z0 + 1) m3_restrict_out<T>(c, j, c.rr + rj * G::RS, c.rr + rj1 * G::RS, c.rr + rj2 * G::RS);
+        if ((j & 1) == 0 && j >= c.z0 + 1)
+            m3_restrict_out<T>(c, j, c.rr + rj * G::RS, c.rr + rj1 * G::RS, c.rr + rj2 * G::RS, R[ic], R[im], R[ip]);
         return;
     }
     if (NM == 2 || j - 1 < c.z0) return;
