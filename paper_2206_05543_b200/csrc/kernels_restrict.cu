@@ -172,9 +172,8 @@ cudaError_t launch_residual_restrict2d_march(const Layout& Lf, const Layout& Lc,
     const int m = Lc.n;
     const int strips = (m + R2<T>::CW - 1) / R2<T>::CW;
     const int slots = num_sms() * occ;
-    int chunks = (slots + strips - 1) / strips;
-    int rows = (m + chunks - 1) / chunks;
-    if (rows < 8) rows = 8;
+    int chunks = march_chunks(strips, slots, m, 8, 1);
+    const int rows = (m + chunks - 1) / chunks;
     chunks = (m + rows - 1) / rows;
     dim3 g(strips, chunks);
     return launch_pdl(k_residual_restrict2d<T>, g, dim3(threads), smem, s, Lf, Lc, x, b, bc, sA, rows);

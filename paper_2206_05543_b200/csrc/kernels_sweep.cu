@@ -448,9 +448,8 @@ static cudaError_t launch_sweep2d_march(const Layout& L, const T* x, const T* b,
     const int W = m2_width<T>();
     const int strips = (L.n + W - 1) / W;
     const int slots = num_sms() * occ;
-    int chunks = (slots + strips - 1) / strips;
-    int rows = (L.n + chunks - 1) / chunks;
-    if (rows < 16) rows = 16;
+    int chunks = march_chunks(strips, slots, L.n, 16, 4);
+    const int rows = (L.n + chunks - 1) / chunks;
     chunks = (L.n + rows - 1) / rows;
     dim3 g(strips, chunks);
     return launch_pdl(k_sweep2d_march<T, S, FZ, NM>, g, dim3(threads), smem, s, L, x, b, xo, M, sA, sM, omega, rows,

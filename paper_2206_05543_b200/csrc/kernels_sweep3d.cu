@@ -432,10 +432,9 @@ cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo,
     }
     const int tx = (L.n + G::TX - 1) / G::TX, ty = (L.n + G::TY - 1) / G::TY;
     const int slots = num_sms() * occ;
-    int chunks = std::max(1, (int)((2LL * slots + tx * ty - 1) / (tx * ty)));  // ~2 waves of marching CTAs
     const int span = NM == 3 ? Lc->n : L.n;  // NM == 3 chunks coarse planes
-    int planes = (span + chunks - 1) / chunks;
-    if (planes < (NM == 3 ? 4 : 8)) planes = NM == 3 ? 4 : 8;
+    int chunks = march_chunks(tx * ty, slots, span, NM == 3 ? 4 : 8, NM == 3 ? 2 : 3);
+    const int planes = (span + chunks - 1) / chunks;
     chunks = (span + planes - 1) / planes;
     dim3 g(tx, ty, chunks);
     return launch_pdl(k_sweep3d_march<T, S, FZ, NM>, g, dim3(M3_THREADS), G::smem, s, L, xm, bm, x, xo, M, sA, sM,

@@ -66,6 +66,29 @@ template <> struct V16<float> {
 template <class T>
 __device__ __forceinline__ void stg16(T* p, const T* v) { V16<T>::st(p, v); }
 
+// Chunk count along the marching axis for `tiles` CTAs per chunk row and `slots` resident CTA
+// slots: favour a whole number of waves (a partial last wave leaves most SMs idle while a few
+// CTAs march their whole chunk) while amortising each chunk's pipeline fill (`fill` extra
+// rows/planes staged per chunk of `len`).
+inline int march_chunks(int tiles, int slots, int span, int min_len, int fill) {
+    int best = 1;
+    double best_e = -1.0;
+    for (int c = 1; c <= span; ++c) {
+        const int len = (span + c - 1) / c;
+        if (len < min_len && c > 1) break;
+        const int cc = (span + len - 1) / len;
+        const long long ctas = (long long)tiles * cc;
+        const long long waves = (ctas + slots - 1) / slots;
+        if (waves > 16) break;
+        const double e = (double)ctas / (double)(waves * slots) * len / (double)(len + fill);
+        if (e > best_e + 1e-9) {
+            best_e = e;
+            best = cc;
+        }
+    }
+    return best;
+}
+
 inline int num_sms() {
     static int sms = 0;
     if (!sms) {
