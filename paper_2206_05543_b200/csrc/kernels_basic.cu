@@ -260,6 +260,20 @@ __global__ void __launch_bounds__(128) k_prolong_correct2d(Layout Lf, Layout Lc,
     const T to0 = e01, to1 = e11;                                           // row 2I+1
     const long long off0 = Lf.origin + (long long)(2 * I) * Lf.px + 2 * J;
     const int nf = Lf.n;
+    // both loads of the (possibly aliased, in-place) fine iterate first, then the stores
+    T xv[2][2] = {};
+    if (acc) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (2 * I + h >= nf) break;
+            const long long off = off0 + (long long)h * Lf.px;
+            if (!lJ) {
+                V16<T>::ld2(xi + off, xv[h]);
+            } else {
+                xv[h][0] = xi[off];
+            }
+        }
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         if (2 * I + h >= nf) break;
@@ -268,19 +282,13 @@ __global__ void __launch_bounds__(128) k_prolong_correct2d(Layout Lf, Layout Lc,
         v[0] = pe<T>(a0, a1, fJ, lJ);  // column 2J
         v[1] = a1;                     // column 2J+1
         const long long off = off0 + (long long)h * Lf.px;
+        T o[2];
+        o[0] = acc ? O::add(xv[h][0], v[0]) : v[0];
+        o[1] = acc ? O::add(xv[h][1], v[1]) : v[1];
         if (!lJ) {
-            T o[2];
-            if (acc) {
-                V16<T>::ld2(xi + off, o);
-                o[0] = O::add(o[0], v[0]);
-                o[1] = O::add(o[1], v[1]);
-            } else {
-                o[0] = v[0];
-                o[1] = v[1];
-            }
             V16<T>::st2(xo + off, o);
         } else {
-            xo[off] = acc ? O::add(xi[off], v[0]) : v[0];
+            xo[off] = o[0];
         }
     }
 }
@@ -310,6 +318,22 @@ __global__ void __launch_bounds__(128) k_prolong_correct3d(Layout Lf, Layout Lc,
     if (K > m) return;
     const bool fI = I == 0, lI = I == m, fJ = J == 0, lJ = J == m, fK = K == 0, lK = K == m;
     const int nf = Lf.n;
+    // all loads of the (possibly aliased, in-place) fine iterate first, then the stores
+    T xv[2][2][2] = {};
+    if (acc) {
+#pragma unroll
+        for (int hi = 0; hi < 2; ++hi)
+#pragma unroll
+            for (int hj = 0; hj < 2; ++hj) {
+                if (2 * I + hi >= nf || 2 * J + hj >= nf) continue;
+                const long long off = Lf.origin + (long long)(2 * I + hi) * Lf.pp + (long long)(2 * J + hj) * Lf.px + 2 * K;
+                if (!lK) {
+                    V16<T>::ld2(xi + off, xv[hi][hj]);
+                } else {
+                    xv[hi][hj][0] = xi[off];
+                }
+            }
+    }
 #pragma unroll
     for (int hi = 0; hi < 2; ++hi) {
         if (2 * I + hi >= nf) break;
@@ -330,19 +354,13 @@ __global__ void __launch_bounds__(128) k_prolong_correct3d(Layout Lf, Layout Lc,
             v[0] = pe<T>(u[0], u[1], fK, lK);  // column 2K
             v[1] = u[1];                       // column 2K+1
             const long long off = Lf.origin + (long long)(2 * I + hi) * Lf.pp + (long long)(2 * J + hj) * Lf.px + 2 * K;
+            T o[2];
+            o[0] = acc ? O::add(xv[hi][hj][0], v[0]) : v[0];
+            o[1] = acc ? O::add(xv[hi][hj][1], v[1]) : v[1];
             if (!lK) {
-                T o[2];
-                if (acc) {
-                    V16<T>::ld2(xi + off, o);
-                    o[0] = O::add(o[0], v[0]);
-                    o[1] = O::add(o[1], v[1]);
-                } else {
-                    o[0] = v[0];
-                    o[1] = v[1];
-                }
                 V16<T>::st2(xo + off, o);
             } else {
-                xo[off] = acc ? O::add(xi[off], v[0]) : v[0];
+                xo[off] = o[0];
             }
         }
     }
