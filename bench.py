@@ -33,6 +33,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HEADLINE = dict(cfg_id="c2", smoother="m9", nu1=1, nu2=1, coarsest_N=2, tol=1e-10)
+# --workload (testing / side runs; the driver's line is c2, BASELINE.json configs[1])
+WORKLOADS = {
+    "c1": ("m9", "c1: 2D Poisson 255^2, sine RHS, m9 SPAI V(1,1), zero start, coarsest h=1/2, tol 1e-10"),
+    "c2": ("m9", "c2: 2D Poisson 4095^2, U[-1,1] seed 0, m9 SPAI V(1,1), zero start, coarsest h=1/2, tol 1e-10"),
+    "c3": ("m7", "c3: 3D Poisson 127^3, sine RHS, m7 SPAI V(1,1), zero start, coarsest h=1/2, tol 1e-10"),
+    "c4": ("m7", "c4: 3D Poisson 511^3, U[-1,1] seed 1, m7 SPAI V(1,1), zero start, coarsest h=1/2, tol 1e-10"),
+}
 METRIC = "V-cycle DOF/s (fp64 SPAI V(1,1))"
 UNIT = "DOF/s"
 FALLBACK_HBM_GBS = 6650.0
@@ -162,15 +169,14 @@ def run_reference(args):
     t = float(np.mean(times))
     value = n0 / t
     cpu = {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-           "sample": f"one {h['smoother']} V({h['nu1']},{h['nu2']}) cycle + residual norm of config 2 "
-                     f"({N - 1}^2, fp64) per step, C restatement of the reference (oracle/), "
+           "sample": f"one {h['smoother']} V({h['nu1']},{h['nu2']}) cycle + residual norm of {h['cfg_id']} "
+                     f"({N - 1}^{dim}, fp64) per step, C restatement of the reference (oracle/), "
                      f"{threads} OpenMP threads"}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "c2: 2D Poisson 4095^2, U[-1,1] seed 0, m9 V(1,1), zero start, coarsest h=1/2",
-                   "sample": "1 cycle/step"},
+        "config": {"workload": WORKLOADS[h["cfg_id"]][1], "sample": "1 cycle/step"},
         "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "host_cpu": _cpu_model(), "host_cpus": os.cpu_count(),
@@ -326,8 +332,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "c2: 2D Poisson 4095^2, U[-1,1] seed 0, m9 SPAI V(1,1), zero start, "
-                                   "coarsest h=1/2, tol 1e-10; step = one solve to tolerance",
+            "config": {"workload": WORKLOADS[h["cfg_id"]][1] + "; step = one solve to tolerance",
                        "l2": "inputs larger than L2 (finest level 134 MB/vector, hierarchy ~0.6 GB)",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
             "cycles_per_solve": cycles_per_step, "time_to_tol_ms": ms_per_step, "ms_per_cycle": t_cycle * 1e3,
@@ -373,7 +378,7 @@ def cpu_baseline_sample():
     t = (time.perf_counter() - t0) / ncyc
     th = c_oracle.max_threads()
     return {"value": (N - 1) ** dim / t, "unit": UNIT, "cores": th, "kind": "port",
-            "sample": f"{ncyc} V(1,1) cycles + norms of config 2 (4095^2 fp64), C restatement, {th} threads",
+            "sample": f"{ncyc} V(1,1) cycles + norms of {h['cfg_id']} ({N - 1}^{dim} fp64), C restatement, {th} threads",
             "s_per_cycle": t, "host_cpu": _cpu_model()}
 
 
@@ -459,7 +464,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     args = ap.parse_args()
+    HEADLINE["cfg_id"] = args.workload
+    HEADLINE["smoother"] = WORKLOADS[args.workload][0]
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -247,3 +247,35 @@ def test_solve_batch_pipelined_matches_single_solves(dim, N, sm):
         assert k == rep.iterations and conv == rep.converged
         assert hist == rep.residual_norms
         assert np.array_equal(u.numpy(), ref_u.values)
+
+
+@pytest.mark.parametrize("env", [{"SPAIMG_NO_GRAPH": "1"}, {"SPAIMG_RESTRICT_V1": "1"}, {"SPAIMG_SWEEP_V1": "1"},
+                                 {"SPAIMG_PDL": "1"}, {"SPAIMG_PC_FLAT": "1"}, {"SPAIMG_TAIL_N": "0"},
+                                 {"SPAIMG_FLAT_N2": "0", "SPAIMG_FLAT_N3": "0", "SPAIMG_PC": "0"}],
+                         ids=lambda e: ",".join(f"{k[7:]}={v}" for k, v in e.items()))
+def test_alternate_paths_bitwise(env):
+    """Every opt-in / fallback kernel path (eager launches, unfused restriction, v1 tile sweeps,
+    PDL, flat K3+K1 fusion, no tail kernel, marching on every level without K3 fusion) gives
+    the same iterations, histories and bitwise iterates as the C oracle."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "env_path_case.py")], capture_output=True,
+                       text=True, timeout=600, env=dict(os.environ, **env))
+    assert r.returncode == 0, r.stderr[-3000:]
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    for case, (cfg_id, sm, gamma, nu1, nu2, cN) in {"c1": ("c1", "m9", 1, 1, 1, 2), "c3": ("c3", "m7", 1, 1, 1, 2),
+                                                    "w64": ("c1", "m9", 2, 1, 0, 4)}.items():
+        b = workloads.rhs(cfg_id)
+        dim, N, _ = workloads.CONFIGS[cfg_id]
+        if case == "w64":
+            N, b = 64, np.random.default_rng(5).uniform(-1, 1, (63, 63))
+        M = sp.named(sm)
+        uo, norms, k, conv = c_oracle.solve_history(b, N, npo.terms_of(M.stencil), M.omega_opt_analytic, nu1, nu2,
+                                                    gamma, cN)
+        it, hist, sha = got[case]
+        assert it == k, (case, it, k)
+        assert max(abs(a - r) / r for a, r in zip(hist, norms)) < 1e-8, case
+        assert sha == hashlib.sha256(uo.tobytes()).hexdigest(), case
