@@ -839,7 +839,49 @@ template <class T> struct Solver final : spaimg_solver {
         return 0;
     }
 
+    // reset; A; check; WHILE(cont) { B; A; check }.  A (norm of u_k fused with the first
+    // pre-sweep of cycle k+1, which only writes the other buffer) is harmlessly speculative
+    // when the check then stops, so no IF node is needed around B (SPAIMG_SOLVE_IF=1 keeps the
+    // reset; WHILE { A; check; IF { B } } form for comparison).
     int build_solve_graph() {
+        const char* ef = getenv("SPAIMG_SOLVE_IF");
+        if (ef && ef[0] == '1') return build_solve_graph_if();
+        cudaGraph_t g;
+        CK(cudaGraphCreate(&g, 0));
+        int launches_a = 0, launches_b = 0, dummy = 0;
+        cudaGraphConditionalHandle hw;
+        cudaGraph_t wbody = nullptr;
+        int rc = 0;
+        cudaError_t e = cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault);
+        if (e != cudaSuccess) rc = fail((int)e, "conditional handle");
+        if (!rc)
+            rc = capture_into(g, [&](cudaStream_t cs) -> int {
+                CK(launch_pdl(k_solve_reset, dim3(1), dim3(1), 0, cs, slot_d, state_d));
+                if (int r = part_a(cs, &dummy)) return r;
+                CK(launch_pdl(k_solve_check, dim3(1), dim3(1), 0, cs, norms_d, slot_d, ctl_d, state_d, hw, hw));
+                return add_conditional(cs, hw, cudaGraphCondTypeWhile, &wbody);
+            });
+        if (!rc)
+            rc = capture_into(wbody, [&](cudaStream_t cs) -> int {
+                if (int r = part_b(cs, &launches_b)) return r;
+                if (int r = part_a(cs, &launches_a)) return r;
+                CK(launch_pdl(k_solve_check, dim3(1), dim3(1), 0, cs, norms_d, slot_d, ctl_d, state_d, hw, hw));
+                ++launches_a;
+                return 0;
+            });
+        if (!rc) {
+            e = cudaGraphInstantiate(&exec_solve, g, 0);
+            if (e != cudaSuccess) rc = fail((int)e, std::string("solve graph instantiate: ") + cudaGetErrorString(e));
+        }
+        cudaGraphDestroy(g);
+        if (!rc) {
+            kernels_per_cycle = launches_a + launches_b;
+            kernels_a = launches_a;
+        }
+        return rc;
+    }
+
+    int build_solve_graph_if() {
         cudaGraph_t g;
         CK(cudaGraphCreate(&g, 0));
         int launches_a = 0, launches_b = 0;
