@@ -279,3 +279,19 @@ def test_alternate_paths_bitwise(env):
         assert it == k, (case, it, k)
         assert max(abs(a - r) / r for a, r in zip(hist, norms)) < 1e-8, case
         assert sha == hashlib.sha256(uo.tobytes()).hexdigest(), case
+
+
+@pytest.mark.parametrize("dim,N,sm", [(2, 256, "m9"), (2, 4096, "m9"), (2, 512, "jacobi2d"), (3, 64, "m7"),
+                                      (3, 256, "m7")])
+def test_fp32_cycles_vs_oracle(dim, N, sm):
+    """fp32 V(1,1) cycles (marching, K3-fused, flat and tail kernels in float32) bitwise against
+    the float32 restatement."""
+    rng = np.random.default_rng(3 * N + dim)
+    x = rng.uniform(-1, 1, (N - 1,) * dim).astype(np.float32)
+    b = rng.uniform(-1, 1, (N - 1,) * dim).astype(np.float32)
+    M = sp.named(sm)
+    cfg = sp.MgConfig(smoother=M, cycle="V", nu1=1, nu2=1, coarsest_N=2)
+    got = host(sp.cycle(sp.Grid(N, dev(x, torch.float32)), sp.Grid(N, dev(b, torch.float32)), cfg))
+    ref = c_oracle.cycle(x, b, N, npo.terms_of(M.stencil), M.omega_opt_analytic, 1, 1, 1, 2, dtype=np.float32)
+    assert got.dtype == np.float32
+    assert np.array_equal(got, ref)
