@@ -101,6 +101,9 @@ struct TailOp {
     int a_in, a_out;  // x buffer indices of the level
     int c;            // PROLONG: x buffer of the coarse level holding the correction
     int fz;           // SWEEP: the input iterate is zero (x not read)
+    int nthr;         // participating threads (a multiple of 32): the op's largest point count
+    int npre;         // threads meeting at the barrier before the op: max(nthr, previous op's nthr)
+    int bid_pre, bid_in;  // named-barrier ids for npre / nthr threads (0 = __syncthreads)
 };
 template <class T> struct TailLevel {
     Layout L;   // compact shared-memory layout (frame = stencil radius)

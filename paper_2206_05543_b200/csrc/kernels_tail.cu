@@ -16,6 +16,8 @@
 //      prolongation reads it there).
 // Every per-point expression is the Appendix-A tree of the multi-kernel path
 // (spaimg_common.cuh), so the tail is bitwise identical to it; only the memory changes.
+#include <cstdlib>
+
 #include "kernels.h"
 #include "march.cuh"
 
@@ -150,13 +152,54 @@ __device__ void tail_prolong_phase(const TailLevel<T>& f, const TailLevel<T>& c,
     }
 }
 
-// getrs order (Appendix A.5/A.6), identical to k_coarse_solve
+// barrier `id` over the first n threads (n a multiple of 32): the small levels of the tail only
+// occupy a few warps, and only those wait for each other.  Warps that skip small ops run ahead
+// to the next barrier that includes them, so every distinct count has its own barrier id (the
+// host assigns them; id 0 = all threads = __syncthreads).
+__device__ __forceinline__ void tbar(int id, int n) {
+    if (id == 0) {
+        __syncthreads();
+    } else {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+    }
+}
+
+// getrs order (Appendix A.5/A.6), identical to k_coarse_solve, in one warp (nlu <= 32): lane i
+// holds y_i; the row interchanges, the column-oriented FMA forward substitution and the
+// true-divide back substitution run in the sequential j order through shuffles
 template <class T>
-__device__ void tail_coarse_phase(const TailLevel<T>& v, T* y, const T* lu, const int* piv, int nlu) {
+__device__ void tail_coarse_warp(const TailLevel<T>& v, const T* lu, const int* piv, int nlu) {
+    using O = Op<T>;
+    const Layout& L = v.L;
+    const int l = threadIdx.x;
+    T y = l < nlu ? v.b[tpoint(L, l)] : T(0);
+    for (int i = 0; i < nlu; ++i) {
+        const int p = piv[i];
+        if (p != i) {
+            const T yi = __shfl_sync(0xffffffffu, y, i), yp = __shfl_sync(0xffffffffu, y, p);
+            if (l == i) y = yp;
+            if (l == p) y = yi;
+        }
+    }
+    for (int j = 0; j < nlu; ++j) {
+        const T yj = __shfl_sync(0xffffffffu, y, j);
+        if (l > j && l < nlu) y = O::fma(-lu[(long long)l * nlu + j], yj, y);
+    }
+    for (int j = nlu - 1; j >= 0; --j) {
+        if (l == j) y = O::div(y, lu[(long long)j * nlu + j]);
+        const T yj = __shfl_sync(0xffffffffu, y, j);
+        if (l < j) y = O::fma(-lu[(long long)l * nlu + j], yj, y);
+    }
+    if (l < nlu) v.x[0][tpoint(L, l)] = y;
+}
+
+// getrs order (Appendix A.5/A.6), identical to k_coarse_solve, over the first n threads
+template <class T>
+__device__ void tail_coarse_phase(const TailLevel<T>& v, T* y, const T* lu, const int* piv, int nlu, int id, int n) {
     using O = Op<T>;
     const Layout& L = v.L;
     for (int q = threadIdx.x; q < nlu; q += blockDim.x) y[q] = v.b[tpoint(L, q)];
-    __syncthreads();
+    tbar(id, n);
     if (threadIdx.x == 0) {
         for (int i = 0; i < nlu; ++i) {
             const int p = piv[i];
@@ -167,18 +210,18 @@ __device__ void tail_coarse_phase(const TailLevel<T>& v, T* y, const T* lu, cons
             }
         }
     }
-    __syncthreads();
+    tbar(id, n);
     for (int j = 0; j < nlu; ++j) {
         const T yj = y[j];
-        for (int i = j + 1 + threadIdx.x; i < nlu; i += blockDim.x) y[i] = O::fma(-lu[(long long)i * nlu + j], yj, y[i]);
-        __syncthreads();
+        for (int i = j + 1 + threadIdx.x; i < nlu; i += n) y[i] = O::fma(-lu[(long long)i * nlu + j], yj, y[i]);
+        tbar(id, n);
     }
     for (int j = nlu - 1; j >= 0; --j) {
         if (threadIdx.x == 0) y[j] = O::div(y[j], lu[(long long)j * nlu + j]);
-        __syncthreads();
+        tbar(id, n);
         const T yj = y[j];
-        for (int i = threadIdx.x; i < j; i += blockDim.x) y[i] = O::fma(-lu[(long long)i * nlu + j], yj, y[i]);
-        __syncthreads();
+        for (int i = threadIdx.x; i < j; i += n) y[i] = O::fma(-lu[(long long)i * nlu + j], yj, y[i]);
+        tbar(id, n);
     }
     for (int q = threadIdx.x; q < nlu; q += blockDim.x) v.x[0][tpoint(L, q)] = y[q];
 }
@@ -213,14 +256,18 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(TailArgs<T> a) {
     // entry level: b (and the start iterate) from its global buffers
     tail_copy<T>(lv[0].L, lv[0].b, a.gL, a.gb);
     if (!a.entry_fz) tail_copy<T>(lv[0].L, lv[0].x[a.entry_a], a.gL, a.gx_in);
+    __syncthreads();
     for (int i = 0; i < a.nops; ++i) {
-        __syncthreads();
         const TailOp op = ops[i];
+        // the threads of op i and of op i-1 (always a prefix of warps) meet here
+        if ((int)threadIdx.x >= op.npre) continue;
+        if (i > 0) tbar(op.bid_pre, op.npre);
+        if ((int)threadIdx.x >= op.nthr) continue;
         const TailLevel<T>& v = lv[op.level];
         switch (op.type) {
             case TAIL_SWEEP:
                 tail_residual_phase<T>(v, v.x[op.a_in], op.fz);
-                __syncthreads();
+                tbar(op.bid_in, op.nthr);
                 tail_relax_phase<T>(v, op.fz ? nullptr : v.x[op.a_in], v.x[op.a_out], a.M, a.omega);
                 break;
             case TAIL_ZERO: {
@@ -230,7 +277,7 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(TailArgs<T> a) {
             }
             case TAIL_RESTRICT:
                 tail_residual_phase<T>(v, v.x[op.a_in], false);
-                __syncthreads();
+                tbar(op.bid_in, op.nthr);
                 tail_restrict_phase<T>(v, lv[op.level + 1]);
                 break;
             case TAIL_PROLONG: {
@@ -239,7 +286,10 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(TailArgs<T> a) {
                 break;
             }
             case TAIL_COARSE:
-                tail_coarse_phase<T>(v, y, a.lu, a.piv, a.nlu);
+                if (a.nlu <= 32)
+                    tail_coarse_warp<T>(v, a.lu, a.piv, a.nlu);
+                else
+                    tail_coarse_phase<T>(v, y, a.lu, a.piv, a.nlu, op.bid_in, op.nthr);
                 break;
         }
     }

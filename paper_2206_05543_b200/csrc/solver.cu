@@ -648,6 +648,7 @@ template <class T> struct Solver final : spaimg_solver {
             for (int fz = 0; fz < 2; ++fz) {
                 std::vector<TailOp> ops;
                 tail_out[a][fz] = record(l0, a, fz != 0, ops);
+                if (int rc = tail_barriers(ops)) return rc;
                 if (int rc = dalloc(&tail_ops[a][fz], ops.size())) return rc;
                 CK(cudaMemcpy(tail_ops[a][fz], ops.data(), ops.size() * sizeof(TailOp), cudaMemcpyHostToDevice));
                 tail_nops[a][fz] = (int)ops.size();
@@ -656,30 +657,61 @@ template <class T> struct Solver final : spaimg_solver {
     }
 
     // the recursion of visit() (multigrid.py:157-185) recorded as tail ops (levels relative to tail_l)
+    // barrier plan of a tail op list: op i waits with the threads of ops i-1 and i; one named
+    // barrier id per distinct thread count (warps skipping small ops run ahead and must not
+    // share a barrier with a different count), id 0 = the whole CTA
+    int tail_barriers(std::vector<TailOp>& ops) {
+        std::vector<int> counts;
+        auto id_of = [&](int n) -> int {
+            if (n >= 1024) return 0;
+            for (size_t k = 0; k < counts.size(); ++k)
+                if (counts[k] == n) return (int)k + 1;
+            counts.push_back(n);
+            return (int)counts.size();
+        };
+        int prev = 1024;
+        for (TailOp& op : ops) {
+            op.npre = std::max(op.nthr, prev);
+            prev = op.nthr;
+            op.bid_pre = id_of(op.npre);
+            op.bid_in = id_of(op.nthr);
+        }
+        if (counts.size() > 15) return fail(SPAIMG_ENOTSUP, "tail: too many distinct level sizes for named barriers");
+        return 0;
+    }
+
+    // threads of a tail op on level l: one per point, whole warps, at most one CTA
+    int tail_threads(int l) const {
+        const long long cnt = count_of(cfg.dim, lv[l].L.N);
+        return (int)std::min<long long>(1024, (cnt + 31) / 32 * 32);
+    }
+
     int record(int l, int a, bool fz, std::vector<TailOp>& ops) {
         const int rl = l - tail_l;
+        const int nt = tail_threads(l);
+        const int nt_coarse = nlu <= 32 ? 32 : (int)std::min(1024, (nlu + 31) / 32 * 32);
         if (l == nsmooth()) {
-            ops.push_back(TailOp{TAIL_COARSE, rl, 0, 0, 0, 0});
+            ops.push_back(TailOp{TAIL_COARSE, rl, 0, 0, 0, 0, nt_coarse});
             return 0;
         }
         for (int k = 0; k < cfg.nu1; ++k) {
-            ops.push_back(TailOp{TAIL_SWEEP, rl, a, 1 - a, 0, fz ? 1 : 0});
+            ops.push_back(TailOp{TAIL_SWEEP, rl, a, 1 - a, 0, fz ? 1 : 0, nt});
             a = 1 - a;
             fz = false;
         }
-        if (fz) ops.push_back(TailOp{TAIL_ZERO, rl, a, a, 0, 0});
-        ops.push_back(TailOp{TAIL_RESTRICT, rl, a, a, 0, 0});
+        if (fz) ops.push_back(TailOp{TAIL_ZERO, rl, a, a, 0, 0, nt});
+        ops.push_back(TailOp{TAIL_RESTRICT, rl, a, a, 0, 0, nt});
         int c;
         if (l + 1 == nsmooth()) {
-            ops.push_back(TailOp{TAIL_COARSE, rl + 1, 0, 0, 0, 0});
+            ops.push_back(TailOp{TAIL_COARSE, rl + 1, 0, 0, 0, 0, nt_coarse});
             c = 0;
         } else {
             c = record(l + 1, 0, true, ops);
             for (int g = 1; g < cfg.gamma; ++g) c = record(l + 1, c, false, ops);
         }
-        ops.push_back(TailOp{TAIL_PROLONG, rl, a, a, c, 0});
+        ops.push_back(TailOp{TAIL_PROLONG, rl, a, a, c, 0, nt});
         for (int k = 0; k < cfg.nu2; ++k) {
-            ops.push_back(TailOp{TAIL_SWEEP, rl, a, 1 - a, 0, 0});
+            ops.push_back(TailOp{TAIL_SWEEP, rl, a, 1 - a, 0, 0, nt});
             a = 1 - a;
         }
         return a;
