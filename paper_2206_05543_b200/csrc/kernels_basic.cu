@@ -234,61 +234,80 @@ __device__ __forceinline__ T pe(T am1, T a0, bool first, bool last) {
     return pl_even<T>(am1, a0, first, last);
 }
 
+// 2D: each thread owns C = 16 / (2 sizeof(T)) consecutive coarse cells (1 in fp64, 2 in fp32), so
+// every fine row segment it writes is one 16-byte vector.
 template <class T>
 __global__ void __launch_bounds__(128) k_prolong_correct2d(Layout Lf, Layout Lc, const T* xi, T* xo,
                                                            const T* __restrict__ e, bool acc) {
     using O = Op<T>;
+    constexpr int C = 16 / (2 * (int)sizeof(T));
+    constexpr int V = 2 * C;  // fine columns per thread
     pdl_wait();
     pdl_trigger();
     const int m = Lc.n;
-    const int J = blockIdx.x * blockDim.x + threadIdx.x;
+    const int J0 = (blockIdx.x * blockDim.x + threadIdx.x) * C;
     const int I = blockIdx.y;
     const int lane = threadIdx.x & 31;
-    // coarse values at rows I-1, I (frame rows are zero) and columns J, J-1
-    const T* ec = e + Lc.origin + (long long)I * Lc.px + J;
-    const T e10 = ec[-Lc.px], e11 = ec[0];           // (I-1, J), (I, J)
-    T e00 = __shfl_up_sync(0xffffffffu, e10, 1);     // (I-1, J-1)
-    T e01 = __shfl_up_sync(0xffffffffu, e11, 1);     // (I, J-1)
-    if (lane == 0) {
-        e00 = ec[-Lc.px - 1];
-        e01 = ec[-1];
+    // coarse rows I-1 (u) and I (d) at columns J0-1 .. J0+C-1 (frames are zero)
+    const T* ec = e + Lc.origin + (long long)I * Lc.px + J0;
+    T eu[C + 1], ed[C + 1];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+        eu[k + 1] = ec[k - Lc.px];
+        ed[k + 1] = ec[k];
     }
-    if (J > m) return;
-    const bool fI = I == 0, lI = I == m, fJ = J == 0, lJ = J == m;
-    // axis 0: interpolants at fine rows 2I (even) and 2I+1 (odd) for coarse columns J-1, J
-    const T te0 = pe<T>(e00, e01, fI, lI), te1 = pe<T>(e10, e11, fI, lI);  // row 2I
-    const T to0 = e01, to1 = e11;                                           // row 2I+1
-    const long long off0 = Lf.origin + (long long)(2 * I) * Lf.px + 2 * J;
+    eu[0] = __shfl_up_sync(0xffffffffu, eu[C], 1);
+    ed[0] = __shfl_up_sync(0xffffffffu, ed[C], 1);
+    if (lane == 0) {
+        eu[0] = ec[-Lc.px - 1];
+        ed[0] = ec[-1];
+    }
+    if (J0 > m) return;
+    const bool fI = I == 0, lI = I == m;
     const int nf = Lf.n;
-    // both loads of the (possibly aliased, in-place) fine iterate first, then the stores
-    T xv[2][2] = {};
+    const long long off0 = Lf.origin + (long long)(2 * I) * Lf.px + 2 * J0;
+    const bool full = 2 * J0 + V <= nf;  // every owned fine column is interior
+    // all loads of the (possibly aliased, in-place) fine iterate first, then the stores
+    T xv[2][V] = {};
     if (acc) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             if (2 * I + h >= nf) break;
-            const long long off = off0 + (long long)h * Lf.px;
-            if (!lJ) {
-                V16<T>::ld2(xi + off, xv[h]);
+            const T* src = xi + off0 + (long long)h * Lf.px;
+            if (full) {
+                V16<T>::ld(src, xv[h]);
             } else {
-                xv[h][0] = xi[off];
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                    if (2 * J0 + v < nf) xv[h][v] = src[v];
             }
         }
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         if (2 * I + h >= nf) break;
-        const T a0 = h ? to0 : te0, a1 = h ? to1 : te1;
-        T v[2];
-        v[0] = pe<T>(a0, a1, fJ, lJ);  // column 2J
-        v[1] = a1;                     // column 2J+1
-        const long long off = off0 + (long long)h * Lf.px;
-        T o[2];
-        o[0] = acc ? O::add(xv[h][0], v[0]) : v[0];
-        o[1] = acc ? O::add(xv[h][1], v[1]) : v[1];
-        if (!lJ) {
-            V16<T>::st2(xo + off, o);
+        // axis 0 at fine row 2I+h for coarse columns J0-1 .. J0+C-1, then axis 1
+        T a[C + 1];
+#pragma unroll
+        for (int k = 0; k <= C; ++k) a[k] = h ? ed[k] : pe<T>(eu[k], ed[k], fI, lI);
+        T o[V];
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            const int J = J0 + k;
+            o[2 * k] = pe<T>(a[k], a[k + 1], J == 0, J == m);  // column 2J
+            o[2 * k + 1] = a[k + 1];                          // column 2J+1
+        }
+        if (acc) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) o[v] = O::add(xv[h][v], o[v]);
+        }
+        T* dst = xo + off0 + (long long)h * Lf.px;
+        if (full) {
+            V16<T>::st(dst, o);
         } else {
-            xo[off] = o[0];
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+                if (2 * J0 + v < nf) dst[v] = o[v];
         }
     }
 }
@@ -371,7 +390,8 @@ cudaError_t launch_prolong_correct(const Layout& Lf, const Layout& Lc, const T* 
                                    bool acc) {
     const int m = Lc.n;
     if (Lf.dim == 2) {
-        dim3 g((m + 1 + 127) / 128, m + 1);
+        constexpr int C = 16 / (2 * (int)sizeof(T));
+        dim3 g(((m + 1 + C - 1) / C + 127) / 128, m + 1);
         return launch_pdl(k_prolong_correct2d<T>, g, dim3(128), 0, s, Lf, Lc, xi, xo, e, acc);
     } else {
         dim3 g((m + 1 + 127) / 128, m + 1, m + 1);

@@ -13,6 +13,13 @@ __global__ void k_empty_pdl(int* p) {
     asm volatile("griddepcontrol.launch_dependents;");
 }
 
+struct Big {
+    double c[96];
+};
+__global__ void k_big(int* p, Big b) {
+    if (threadIdx.x == 0 && blockIdx.x == 0 && p && b.c[5] > 1e300) atomicAdd(p, 1);
+}
+
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -130,6 +137,49 @@ int main() {
         CK(cudaGraphInstantiate(&ge, g, 0));
         float ms = time_graph(ge, s, 20);
         printf("WHILE body (10 iters x 11 kernels, 148 CTAs): %.3f us per kernel\n", ms * 1e3 / 110);
+    }
+    // 768-byte kernel parameters: flat chain and inside a WHILE body
+    {
+        Big bg{};
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        for (int i = 0; i < K; ++i) k_big<<<148, 256, 0, s>>>(nullptr, bg);
+        CK(cudaStreamEndCapture(s, &g));
+        cudaGraphExec_t ge;
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        printf("chain of %d 768-B-param kernels, 148 CTAs: %.3f us per kernel\n", K, time_graph(ge, s, 20) * 1e3 / K);
+    }
+    {
+        Big bg{};
+        cudaGraph_t g;
+        CK(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle h;
+        CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams p{};
+        p.type = cudaGraphNodeTypeConditional;
+        p.conditional.handle = h;
+        p.conditional.type = cudaGraphCondTypeWhile;
+        p.conditional.size = 1;
+        cudaGraphNode_t nset, ncond;
+        cudaKernelNodeParams kp{};
+        int v = 10;
+        void* args_set[] = {&d, &v};
+        kp.func = (void*)k_set;
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(1);
+        kp.kernelParams = args_set;
+        CK(cudaGraphAddKernelNode(&nset, g, nullptr, 0, &kp));
+        CK(cudaGraphAddNode(&ncond, g, &nset, 1, &p));
+        cudaGraph_t body = p.conditional.phGraph_out[0];
+        cudaStream_t cs;
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        for (int i = 0; i < 30; ++i) k_big<<<148, 256, 0, cs>>>(nullptr, bg);
+        k_dec<<<1, 1, 0, cs>>>(d, h);
+        CK(cudaStreamEndCapture(cs, &body));
+        cudaGraphExec_t ge;
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        printf("WHILE body (10 iters x 31 kernels, 768-B params): %.3f us per kernel\n", time_graph(ge, s, 20) * 1e3 / 310);
     }
     // grid barrier cost
     unsigned* bar;
