@@ -312,74 +312,88 @@ __global__ void __launch_bounds__(128) k_prolong_correct2d(Layout Lf, Layout Lc,
     }
 }
 
+// 3D: each thread owns C = 16 / (2 sizeof(T)) consecutive coarse cells along axis 2.
 template <class T>
 __global__ void __launch_bounds__(128) k_prolong_correct3d(Layout Lf, Layout Lc, const T* xi, T* xo,
                                                            const T* __restrict__ e, bool acc) {
     using O = Op<T>;
+    constexpr int C = 16 / (2 * (int)sizeof(T));
+    constexpr int V = 2 * C;
     pdl_wait();
     pdl_trigger();
     const int m = Lc.n;
-    const int K = blockIdx.x * blockDim.x + threadIdx.x;
+    const int K0 = (blockIdx.x * blockDim.x + threadIdx.x) * C;
     const int J = blockIdx.y, I = blockIdx.z;
     const int lane = threadIdx.x & 31;
-    // c[di][dj][dk]: coarse value at (I-1+di, J-1+dj, K-1+dk)
-    T c[2][2][2];
-    const T* ec = e + Lc.origin + (long long)I * Lc.pp + (long long)J * Lc.px + K;
+    // c[di][dj][k]: coarse value at (I-1+di, J-1+dj, K0-1+k), k = 0..C (frames are zero)
+    T c[2][2][C + 1];
+    const T* ec = e + Lc.origin + (long long)I * Lc.pp + (long long)J * Lc.px + K0;
 #pragma unroll
     for (int di = 0; di < 2; ++di)
 #pragma unroll
         for (int dj = 0; dj < 2; ++dj) {
             const T* q = ec + (long long)(di - 1) * Lc.pp + (long long)(dj - 1) * Lc.px;
-            c[di][dj][1] = q[0];
-            c[di][dj][0] = __shfl_up_sync(0xffffffffu, c[di][dj][1], 1);
+#pragma unroll
+            for (int k = 0; k < C; ++k) c[di][dj][k + 1] = q[k];
+            c[di][dj][0] = __shfl_up_sync(0xffffffffu, c[di][dj][C], 1);
             if (lane == 0) c[di][dj][0] = q[-1];
         }
-    if (K > m) return;
-    const bool fI = I == 0, lI = I == m, fJ = J == 0, lJ = J == m, fK = K == 0, lK = K == m;
+    if (K0 > m) return;
+    const bool fI = I == 0, lI = I == m, fJ = J == 0, lJ = J == m;
     const int nf = Lf.n;
+    const bool full = 2 * K0 + V <= nf;
     // all loads of the (possibly aliased, in-place) fine iterate first, then the stores
-    T xv[2][2][2] = {};
+    T xv[2][2][V] = {};
     if (acc) {
 #pragma unroll
         for (int hi = 0; hi < 2; ++hi)
 #pragma unroll
             for (int hj = 0; hj < 2; ++hj) {
                 if (2 * I + hi >= nf || 2 * J + hj >= nf) continue;
-                const long long off = Lf.origin + (long long)(2 * I + hi) * Lf.pp + (long long)(2 * J + hj) * Lf.px + 2 * K;
-                if (!lK) {
-                    V16<T>::ld2(xi + off, xv[hi][hj]);
+                const T* src = xi + Lf.origin + (long long)(2 * I + hi) * Lf.pp + (long long)(2 * J + hj) * Lf.px + 2 * K0;
+                if (full) {
+                    V16<T>::ld(src, xv[hi][hj]);
                 } else {
-                    xv[hi][hj][0] = xi[off];
+#pragma unroll
+                    for (int v = 0; v < V; ++v)
+                        if (2 * K0 + v < nf) xv[hi][hj][v] = src[v];
                 }
             }
     }
 #pragma unroll
     for (int hi = 0; hi < 2; ++hi) {
         if (2 * I + hi >= nf) break;
-        // axis 0 at fine plane 2I+hi, coarse (J-1+dj, K-1+dk)
-        T t[2][2];
+        // axis 0 at fine plane 2I+hi, coarse (J-1+dj, K0-1+k)
+        T t[2][C + 1];
 #pragma unroll
         for (int dj = 0; dj < 2; ++dj)
 #pragma unroll
-            for (int dk = 0; dk < 2; ++dk) t[dj][dk] = hi ? c[1][dj][dk] : pe<T>(c[0][dj][dk], c[1][dj][dk], fI, lI);
+            for (int k = 0; k <= C; ++k) t[dj][k] = hi ? c[1][dj][k] : pe<T>(c[0][dj][k], c[1][dj][k], fI, lI);
 #pragma unroll
         for (int hj = 0; hj < 2; ++hj) {
             if (2 * J + hj >= nf) break;
-            // axis 1 at fine row 2J+hj, coarse K-1+dk
-            T u[2];
+            // axis 1 at fine row 2J+hj, then axis 2
+            T u[C + 1];
 #pragma unroll
-            for (int dk = 0; dk < 2; ++dk) u[dk] = hj ? t[1][dk] : pe<T>(t[0][dk], t[1][dk], fJ, lJ);
-            T v[2];
-            v[0] = pe<T>(u[0], u[1], fK, lK);  // column 2K
-            v[1] = u[1];                       // column 2K+1
-            const long long off = Lf.origin + (long long)(2 * I + hi) * Lf.pp + (long long)(2 * J + hj) * Lf.px + 2 * K;
-            T o[2];
-            o[0] = acc ? O::add(xv[hi][hj][0], v[0]) : v[0];
-            o[1] = acc ? O::add(xv[hi][hj][1], v[1]) : v[1];
-            if (!lK) {
-                V16<T>::st2(xo + off, o);
+            for (int k = 0; k <= C; ++k) u[k] = hj ? t[1][k] : pe<T>(t[0][k], t[1][k], fJ, lJ);
+            T o[V];
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                const int K = K0 + k;
+                o[2 * k] = pe<T>(u[k], u[k + 1], K == 0, K == m);  // column 2K
+                o[2 * k + 1] = u[k + 1];                          // column 2K+1
+            }
+            if (acc) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) o[v] = O::add(xv[hi][hj][v], o[v]);
+            }
+            T* dst = xo + Lf.origin + (long long)(2 * I + hi) * Lf.pp + (long long)(2 * J + hj) * Lf.px + 2 * K0;
+            if (full) {
+                V16<T>::st(dst, o);
             } else {
-                xo[off] = o[0];
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                    if (2 * K0 + v < nf) dst[v] = o[v];
             }
         }
     }
@@ -394,7 +408,8 @@ cudaError_t launch_prolong_correct(const Layout& Lf, const Layout& Lc, const T* 
         dim3 g(((m + 1 + C - 1) / C + 127) / 128, m + 1);
         return launch_pdl(k_prolong_correct2d<T>, g, dim3(128), 0, s, Lf, Lc, xi, xo, e, acc);
     } else {
-        dim3 g((m + 1 + 127) / 128, m + 1, m + 1);
+        constexpr int C = 16 / (2 * (int)sizeof(T));
+        dim3 g(((m + 1 + C - 1) / C + 127) / 128, m + 1, m + 1);
         return launch_pdl(k_prolong_correct3d<T>, g, dim3(128), 0, s, Lf, Lc, xi, xo, e, acc);
     }
     return cudaGetLastError();
