@@ -206,7 +206,11 @@ def _custom_stencils(dim):
     box = {}
     for k, o in enumerate(itertools.product((0, 1, -1), repeat=dim)):
         box[o] = Fraction(1, 7 + k) if any(o) else Fraction(3, 4)
-    return {"reversed": (rev, 0.15), "box": (sp.Stencil(dim, box, 2), 0.05)}
+    # radius 2 (the unfused residual + relax path, and a 2-cell frame in the tail)
+    far = {o: c for o, c in base.entries.items()}
+    far[(2,) + (0,) * (dim - 1)] = Fraction(1, 50)
+    far[(0,) * (dim - 1) + (-2,)] = Fraction(1, 40)
+    return {"reversed": (rev, 0.15), "box": (sp.Stencil(dim, box, 2), 0.05), "radius2": (sp.Stencil(dim, far, 2), 0.1)}
 
 
 @pytest.mark.parametrize("dim,N", [(2, 66), (3, 34)])
