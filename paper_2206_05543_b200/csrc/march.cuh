@@ -139,9 +139,17 @@ __device__ __forceinline__ void norm_epilogue(double s, const NormOut& no) {
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
         if (l == 0) {
             const int sl = *no.slot;
-            no.norms[sl] = sqrt(t);
+            const double nrm = sqrt(t);
+            no.norms[sl] = nrm;
             *no.slot = sl + 1;
             *no.counter = 0u;
+            if (no.ctl) {  // k = sl cycles done; the k_solve_check logic
+                const bool conv = sl >= 1 && nrm <= no.ctl->tol * no.norms[0];
+                const bool cont = !conv && sl < no.ctl->max_iters;
+                no.state[0] = sl;
+                no.state[1] = conv ? 1 : 0;
+                cudaGraphSetConditional(no.cond, cont ? 1u : 0u);
+            }
         }
     }
 }

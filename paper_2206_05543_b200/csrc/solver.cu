@@ -399,11 +399,6 @@ struct spaimg_solver {
 //                                 IF(cont) { B: rest of cycle k+1 } }
 // No host round trip per cycle; the history stays on the device until the loop ends.
 // ------------------------------------------------------------------------------------------
-struct SolveCtl {
-    double tol;
-    int max_iters;
-    int pad;
-};
 
 __global__ void k_solve_reset(int* slot, int* state) {
     pdl_wait();
@@ -498,7 +493,13 @@ template <class T> struct Solver final : spaimg_solver {
         return 0;
     }
 
-    NormOut norm_sink() const { return NormOut{partials, counter, norms_d, slot_d}; }
+    NormOut norm_sink() const { return NormOut{partials, counter, norms_d, slot_d, nullptr, nullptr, 0}; }
+    // the norm sink that also evaluates the stop test and drives the WHILE node (solve graph)
+    NormOut norm_sink_cond(cudaGraphConditionalHandle h) const {
+        return NormOut{partials, counter, norms_d, slot_d, ctl_d, state_d, h};
+    }
+    cudaGraphConditionalHandle cur_cond = 0;  // set while capturing the solve graph (fold mode)
+    bool fold_check = false;
 
     int init(const spaimg_mg_config& c) {
         cfg = c;
@@ -750,7 +751,7 @@ template <class T> struct Solver final : spaimg_solver {
     int norm_launch(const T* x, cudaStream_t s, int* launches) {
         const Level<T>& L = lv[0];
         if (sweep_norm_supported()) {
-            CK(launch_norm_march<T>(L.L, x, L.b, L.sA, norm_sink(), s));
+            CK(launch_norm_march<T>(L.L, x, L.b, L.sA, fold_check ? norm_sink_cond(cur_cond) : norm_sink(), s));
         } else {
             CK(launch_residual_norm<T>(L.L, x, L.b, L.sA, partials, counter, norms_d, 0, slot_d, s));
         }
@@ -819,7 +820,7 @@ template <class T> struct Solver final : spaimg_solver {
     int part_a(cudaStream_t s, int* launches) {
         if (fused_norm) {
             Level<T>& L = lv[0];
-            const NormOut no = norm_sink();
+            const NormOut no = fold_check ? norm_sink_cond(cur_cond) : norm_sink();
             CK(launch_sweep<T>(L.L, L.x[0], L.b, L.x[1], M, shape, L.sA, L.sM, omega, false, s, &no));
             ++*launches;
             return 0;
@@ -886,21 +887,30 @@ template <class T> struct Solver final : spaimg_solver {
         int rc = 0;
         cudaError_t e = cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault);
         if (e != cudaSuccess) rc = fail((int)e, "conditional handle");
+        // the stop test rides in the norm's last CTA (no separate check node) when the norm
+        // comes from the marching kernels (SPAIMG_FOLD_CHECK=0 keeps the check kernel)
+        const char* ef2 = getenv("SPAIMG_FOLD_CHECK");
+        fold_check = sweep_norm_supported() && !(ef2 && ef2[0] == '0');
+        cur_cond = hw;
         if (!rc)
             rc = capture_into(g, [&](cudaStream_t cs) -> int {
                 CK(launch_pdl(k_solve_reset, dim3(1), dim3(1), 0, cs, slot_d, state_d));
                 if (int r = part_a(cs, &dummy)) return r;
-                CK(launch_pdl(k_solve_check, dim3(1), dim3(1), 0, cs, norms_d, slot_d, ctl_d, state_d, hw, hw));
+                if (!fold_check)
+                    CK(launch_pdl(k_solve_check, dim3(1), dim3(1), 0, cs, norms_d, slot_d, ctl_d, state_d, hw, hw));
                 return add_conditional(cs, hw, cudaGraphCondTypeWhile, &wbody);
             });
         if (!rc)
             rc = capture_into(wbody, [&](cudaStream_t cs) -> int {
                 if (int r = part_b(cs, &launches_b)) return r;
                 if (int r = part_a(cs, &launches_a)) return r;
-                CK(launch_pdl(k_solve_check, dim3(1), dim3(1), 0, cs, norms_d, slot_d, ctl_d, state_d, hw, hw));
-                ++launches_a;
+                if (!fold_check) {
+                    CK(launch_pdl(k_solve_check, dim3(1), dim3(1), 0, cs, norms_d, slot_d, ctl_d, state_d, hw, hw));
+                    ++launches_a;
+                }
                 return 0;
             });
+        fold_check = false;
         if (!rc) {
             e = cudaGraphInstantiate(&exec_solve, g, 0);
             if (e != cudaSuccess) rc = fail((int)e, std::string("solve graph instantiate: ") + cudaGetErrorString(e));

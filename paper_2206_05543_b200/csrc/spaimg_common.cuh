@@ -114,11 +114,23 @@ template <> struct ShapeT<SHAPE_STAR7> {
 };
 
 // Device-side residual-history sink of the fused norm (see march.cuh norm_epilogue).
+// Stop test of the reference solve loop (multigrid.py:211-217) evaluated on the device.
+struct SolveCtl {
+    double tol;
+    int max_iters;
+    int pad;
+};
+
 struct NormOut {
     double* partials;   // >= number of CTAs
     unsigned* counter;  // zero on entry, re-armed to zero by the last CTA
     double* norms;      // residual history
     int* slot;          // history cursor
+    // optional (ctl != nullptr): the last CTA also runs the stop test on the new norm and sets
+    // the solve loop's WHILE condition (state = {cycles done, converged})
+    const SolveCtl* ctl;
+    int* state;
+    cudaGraphConditionalHandle cond;
 };
 
 // ------------------------------------------------------------------------------------------
