@@ -68,6 +68,11 @@ cudaError_t launch_residual_restrict(const Layout& Lf, const Layout& Lc, const T
 // K2 / K1 for small levels: flat one-wave kernels (kernels_flat.cu); levels with mesh count
 // N <= flat_threshold(dim) use them instead of the marching kernels
 int flat_threshold(int dim);
+// K2 fused with the coarse level's first (zero-start) pre-sweep: bc = restrict(b - A x),
+// xc = 0 + omega (M bc) sMc  (radius-1 M; small levels)
+template <class T>
+cudaError_t launch_residual_restrict_fz(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T* xc,
+                                        const Terms<T>& M, int shape, T sA, T sMc, T omega, cudaStream_t s);
 template <class T>
 cudaError_t launch_sweep_pc_flat(const Layout& L, const Layout& Lc, const T* x, const T* e, const T* b, T* xo,
                                  const Terms<T>& M, int shape, T sA, T sM, T omega, cudaStream_t s);

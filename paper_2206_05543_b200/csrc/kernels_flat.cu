@@ -90,6 +90,176 @@ __global__ void __launch_bounds__(256) k_rr3d_flat(Layout Lf, Layout Lc, const T
 }
 
 // ------------------------------------------------------------------------------------------
+// K2 + the coarse level's first pre-sweep from zero, for the small levels: the coarse right-
+// hand side bc = restrict(b - A x) is formed on the coarse tile plus a one-point ring (the
+// ring recomputed from the fine footprint), and the coarse level's zero-start sweep
+// xc' = 0 + omega ((M bc) sM) (r = b - A 0 = b exactly, multigrid.py:99-100) is applied to the
+// tile in the same pass.  One launch per level on the way down instead of two.
+// ------------------------------------------------------------------------------------------
+template <class T, int S>
+__global__ void __launch_bounds__(256) k_rr2d_flat_fz(Layout Lf, Layout Lc, const T* __restrict__ x,
+                                                      const T* __restrict__ b, T* __restrict__ bc,
+                                                      T* __restrict__ xc, Terms<T> M, T sA, T sMc, T omega) {
+    using O = Op<T>;
+    constexpr int BH = F2_CH + 2, BW = F2_CW + 2;          // coarse tile + ring
+    constexpr int RH = 2 * BH + 1, RW = 2 * BW + 1, RP = RW + 1;  // fine r footprint
+    __shared__ T rs[RH * RP];
+    __shared__ T bs[BH * BW];
+    pdl_wait();
+    pdl_trigger();
+    const int n = Lf.n, m = Lc.n;
+    const int I0 = blockIdx.y * F2_CH - 1, J0 = blockIdx.x * F2_CW - 1;  // ring origin (coarse)
+    const int f0 = 2 * I0, g0 = 2 * J0;
+    for (int q = threadIdx.x; q < RH * RW; q += blockDim.x) {
+        const int lr = q / RW, lc = q - lr * RW;
+        const int i0 = f0 + lr, i1 = g0 + lc;
+        T rv = T(0);
+        if (i0 >= 0 && i0 < n && i1 >= 0 && i1 < n) {
+            const long long p = Lf.origin + (long long)i0 * Lf.px + i1;
+            rv = residual2d<T>(b[p], x[p], x[p + Lf.px], x[p - Lf.px], x[p + 1], x[p - 1], sA);
+        }
+        rs[lr * RP + lc] = rv;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < BH * BW; q += blockDim.x) {
+        const int yc = q / BW, xc_ = q - yc * BW;
+        const int I = I0 + yc, K = J0 + xc_;
+        T v = T(0);  // r = b on the coarse interior, 0 outside (zero start)
+        if (I >= 0 && I < m && K >= 0 && K < m) {
+            T t[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const int c = 2 * xc_ + a;
+                t[a] = fw<T>(rs[(2 * yc) * RP + c], rs[(2 * yc + 1) * RP + c], rs[(2 * yc + 2) * RP + c]);
+            }
+            v = fw<T>(t[0], t[1], t[2]);
+        }
+        bs[q] = v;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < F2_CH * F2_CW; q += blockDim.x) {
+        const int yc = q / F2_CW + 1, xc_ = q % F2_CW + 1;
+        const int I = I0 + yc, K = J0 + xc_;
+        if (I >= m || K >= m) continue;
+        T acc = T(0);
+        const int nt = tnt<T, S>(M);
+#pragma unroll
+        for (int k = 0; k < (S == SHAPE_GENERIC ? kMaxTerms : ShapeT<(S == SHAPE_GENERIC ? 1 : S)>::nt); ++k) {
+            if (S == SHAPE_GENERIC && k >= nt) break;
+            acc = O::add(acc, O::mul(M.c[k], bs[(yc + toff<T, S>(M, k, 0)) * BW + xc_ + toff<T, S>(M, k, 1)]));
+        }
+        const long long pc = Lc.origin + (long long)I * Lc.px + K;
+        bc[pc] = bs[yc * BW + xc_];
+        xc[pc] = relax<T>(T(0), acc, sMc, omega);
+    }
+}
+
+template <class T, int S>
+__global__ void __launch_bounds__(256) k_rr3d_flat_fz(Layout Lf, Layout Lc, const T* __restrict__ x,
+                                                      const T* __restrict__ b, T* __restrict__ bc,
+                                                      T* __restrict__ xc, Terms<T> M, T sA, T sMc, T omega) {
+    using O = Op<T>;
+    constexpr int CZ = 2, CY = 4, CX = 16;                   // coarse tile (128 outputs)
+    constexpr int BZ = CZ + 2, BY = CY + 2, BX = CX + 2;     // + ring
+    constexpr int RZ = 2 * BZ + 1, RY = 2 * BY + 1, RX = 2 * BX + 1, RP = RX + 1;
+    __shared__ T rs[RZ * RY * RP];
+    __shared__ T bs[BZ * BY * BX];
+    pdl_wait();
+    pdl_trigger();
+    const int n = Lf.n, m = Lc.n;
+    const int I0 = blockIdx.z * CZ - 1, J0 = blockIdx.y * CY - 1, K0 = blockIdx.x * CX - 1;
+    const int f0 = 2 * I0, f1 = 2 * J0, f2 = 2 * K0;
+    for (int q = threadIdx.x; q < RZ * RY * RX; q += blockDim.x) {
+        const int lz = q / (RY * RX), rem = q - lz * RY * RX, ly = rem / RX, lx = rem - ly * RX;
+        const int i0 = f0 + lz, i1 = f1 + ly, i2 = f2 + lx;
+        T rv = T(0);
+        if (i0 >= 0 && i0 < n && i1 >= 0 && i1 < n && i2 >= 0 && i2 < n) {
+            const long long p = Lf.origin + (long long)i0 * Lf.pp + (long long)i1 * Lf.px + i2;
+            rv = residual3d<T>(b[p], x[p], x[p + Lf.pp], x[p - Lf.pp], x[p + Lf.px], x[p - Lf.px], x[p + 1], x[p - 1],
+                               sA);
+        }
+        rs[(lz * RY + ly) * RP + lx] = rv;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < BZ * BY * BX; q += blockDim.x) {
+        const int zc = q / (BY * BX), yc = (q / BX) % BY, xc_ = q % BX;
+        const int I = I0 + zc, J = J0 + yc, K = K0 + xc_;
+        T v = T(0);
+        if (I >= 0 && I < m && J >= 0 && J < m && K >= 0 && K < m) {
+            T u[3];
+#pragma unroll
+            for (int qk = 0; qk < 3; ++qk) {
+                T t[3];
+#pragma unroll
+                for (int qj = 0; qj < 3; ++qj) {
+                    const int o = (2 * yc + qj) * RP + 2 * xc_ + qk;
+                    t[qj] = fw<T>(rs[(2 * zc) * RY * RP + o], rs[(2 * zc + 1) * RY * RP + o],
+                                  rs[(2 * zc + 2) * RY * RP + o]);
+                }
+                u[qk] = fw<T>(t[0], t[1], t[2]);
+            }
+            v = fw<T>(u[0], u[1], u[2]);
+        }
+        bs[q] = v;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < CZ * CY * CX; q += blockDim.x) {
+        const int zc = q / (CY * CX) + 1, yc = (q / CX) % CY + 1, xc_ = q % CX + 1;
+        const int I = I0 + zc, J = J0 + yc, K = K0 + xc_;
+        if (I >= m || J >= m || K >= m) continue;
+        T acc = T(0);
+        const int nt = tnt<T, S>(M);
+#pragma unroll
+        for (int k = 0; k < (S == SHAPE_GENERIC ? kMaxTerms : ShapeT<(S == SHAPE_GENERIC ? 1 : S)>::nt); ++k) {
+            if (S == SHAPE_GENERIC && k >= nt) break;
+            const int o0 = toff<T, S>(M, k, 0), o1 = toff<T, S>(M, k, 1), o2 = toff<T, S>(M, k, 2);
+            acc = O::add(acc, O::mul(M.c[k], bs[((zc + o0) * BY + yc + o1) * BX + xc_ + o2]));
+        }
+        const long long pc = Lc.origin + (long long)I * Lc.pp + (long long)J * Lc.px + K;
+        bc[pc] = bs[(zc * BY + yc) * BX + xc_];
+        xc[pc] = relax<T>(T(0), acc, sMc, omega);
+    }
+}
+
+template <class T, int S>
+static cudaError_t rr_fz(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T* xc,
+                         const Terms<T>& M, T sA, T sMc, T omega, cudaStream_t s) {
+    const int m = Lc.n;
+    if (Lf.dim == 2) {
+        dim3 g((m + F2_CW - 1) / F2_CW, (m + F2_CH - 1) / F2_CH);
+        return launch_pdl(k_rr2d_flat_fz<T, S>, g, dim3(256), 0, s, Lf, Lc, x, b, bc, xc, M, sA, sMc, omega);
+    }
+    dim3 g((m + 15) / 16, (m + 3) / 4, (m + 1) / 2);
+    return launch_pdl(k_rr3d_flat_fz<T, S>, g, dim3(128), 0, s, Lf, Lc, x, b, bc, xc, M, sA, sMc, omega);
+}
+
+template <class T>
+cudaError_t launch_residual_restrict_fz(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T* xc,
+                                        const Terms<T>& M, int shape, T sA, T sMc, T omega, cudaStream_t s) {
+    switch (shape) {
+        case SHAPE_C1: return rr_fz<T, SHAPE_C1>(Lf, Lc, x, b, bc, xc, M, sA, sMc, omega, s);
+        case SHAPE_STAR5:
+            if (Lf.dim == 2) return rr_fz<T, SHAPE_STAR5>(Lf, Lc, x, b, bc, xc, M, sA, sMc, omega, s);
+            break;
+        case SHAPE_BOX9:
+            if (Lf.dim == 2) return rr_fz<T, SHAPE_BOX9>(Lf, Lc, x, b, bc, xc, M, sA, sMc, omega, s);
+            break;
+        case SHAPE_STAR7:
+            if (Lf.dim == 3) return rr_fz<T, SHAPE_STAR7>(Lf, Lc, x, b, bc, xc, M, sA, sMc, omega, s);
+            break;
+        default: break;
+    }
+    return rr_fz<T, SHAPE_GENERIC>(Lf, Lc, x, b, bc, xc, M, sA, sMc, omega, s);
+}
+
+template cudaError_t launch_residual_restrict_fz<double>(const Layout&, const Layout&, const double*, const double*,
+                                                         double*, double*, const Terms<double>&, int, double, double,
+                                                         double, cudaStream_t);
+template cudaError_t launch_residual_restrict_fz<float>(const Layout&, const Layout&, const float*, const float*,
+                                                        float*, float*, const Terms<float>&, int, float, float, float,
+                                                        cudaStream_t);
+
+// ------------------------------------------------------------------------------------------
 // K3 + K1 for the small levels: xo = sweep(x + P e) in one flat tile kernel.  The corrected
 // iterate xc = x + P e (multigrid.py:184; k_prolong_correct2d/3d trees) is formed on the tile
 // plus a 2-point halo in shared memory, r = b - A xc on the tile plus a 1-point halo, then

@@ -759,8 +759,15 @@ template <class T> struct Solver final : spaimg_solver {
         return 0;
     }
 
+    static bool rrfz_enabled(int dim) {
+        const char* e = getenv("SPAIMG_RRFZ");
+        if (e) return e[0] == '1';
+        return dim == 2;
+    }
+
     // recursive schedule (multigrid.py:157-185).  Returns the buffer index of level l holding
-    // the result, or -1 on error.  pre_done: the first pre-sweep of level 0 already ran (A).
+    // the result, or -1 on error.  pre_done: the first pre-sweep already ran (level 0: part A;
+    // small levels: fused into the finer level's residual + restriction kernel).
     int visit(int l, int a, bool fz, cudaStream_t s, int* launches, bool pre_done) {
         if (l >= tail_l && l < nsmooth()) return tail_visit(l, a, fz, s, launches);
         Level<T>& L = lv[l];
@@ -770,7 +777,7 @@ template <class T> struct Solver final : spaimg_solver {
             return 0;
         }
         for (int k = 0; k < cfg.nu1; ++k) {
-            if (!(l == 0 && pre_done && k == 0))
+            if (!(pre_done && k == 0))
                 if (do_sweep<T>(L, a, fz, M, shape, fused, omega, s, launches)) return -1;
             a = 1 - a;
             fz = false;
@@ -780,15 +787,27 @@ template <class T> struct Solver final : spaimg_solver {
             ++*launches;
         }
         Level<T>& C = lv[l + 1];
-        if (launch_residual_restrict<T>(L.L, C.L, L.x[a], L.b, C.b, L.sA, L.r, s) != cudaSuccess) return -1;
-        *launches += residual_restrict_launches(cfg.dim);
+        // on the small 2D levels the coarse level's first (zero-start) pre-sweep rides with K2
+        // (measured: c2 -1.7 %, c1 -3.5 %; in 3D the ring recomputation costs more than the
+        // launch it saves, c3 +7 %, so 3D keeps two kernels unless SPAIMG_RRFZ=1)
+        const bool rr_fz = fused && cfg.nu1 >= 1 && l + 1 < nsmooth() && l + 1 < tail_l &&
+                           L.L.N <= flat_threshold(cfg.dim) && !getenv("SPAIMG_RESTRICT_V1") && rrfz_enabled(cfg.dim);
+        if (rr_fz) {
+            if (launch_residual_restrict_fz<T>(L.L, C.L, L.x[a], L.b, C.b, C.x[1], M, shape, L.sA, C.sM, omega, s) !=
+                cudaSuccess)
+                return -1;
+            ++*launches;
+        } else {
+            if (launch_residual_restrict<T>(L.L, C.L, L.x[a], L.b, C.b, L.sA, L.r, s) != cudaSuccess) return -1;
+            *launches += residual_restrict_launches(cfg.dim);
+        }
         int c;
         if (l + 1 == nsmooth()) {
             if (launch_coarse_solve<T>(C.L, C.b, C.x[0], lu, piv, nlu, s) != cudaSuccess) return -1;
             ++*launches;
             c = 0;
         } else {
-            c = visit(l + 1, 0, true, s, launches, false);
+            c = visit(l + 1, 0, true, s, launches, rr_fz);
             for (int g = 1; g < cfg.gamma && c >= 0; ++g) c = visit(l + 1, c, false, s, launches, false);
             if (c < 0) return -1;
         }
