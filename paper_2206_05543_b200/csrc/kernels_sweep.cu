@@ -432,12 +432,10 @@ static cudaError_t launch_sweep2d_march(const Layout& L, const T* x, const T* b,
                                         T sM, T omega, const NormOut& no, cudaStream_t s, const T* e = nullptr,
                                         const Layout* Lc = nullptr) {
     constexpr size_t smem = m2_smem_bytes<T>(NM == 3);
-    static bool attr = false;
-    if (!attr && smem > 48 * 1024) {
+    if (smem > 48 * 1024) {  // per device, so set on every launch (host-side, cheap)
         cudaError_t err = cudaFuncSetAttribute(k_sweep2d_march<T, S, FZ, NM>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (err != cudaSuccess) return err;
-        attr = true;
     }
     constexpr int threads = (M2_NW + 1) * 32;
     static int occ = 0;

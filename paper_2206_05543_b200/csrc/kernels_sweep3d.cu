@@ -411,12 +411,10 @@ template <class T, int S, bool FZ, int NM>
 cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
                                  T omega, const NormOut& no, cudaStream_t s, const Layout* Lc) {
     using G = M3<T>;
-    static bool attr = false;
-    if (!attr) {
+    {  // per device, so set on every launch (host-side, cheap)
         cudaError_t e = cudaFuncSetAttribute(k_sweep3d_march<T, S, FZ, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)G::smem);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     // base pointers of the allocations (the layout origin is an offset into them)
     const T* xbase = x ? x : b;  // FZ never reads x; any valid map works

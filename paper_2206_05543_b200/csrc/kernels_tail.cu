@@ -299,11 +299,9 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(TailArgs<T> a) {
 
 template <class T>
 cudaError_t launch_tail(const TailArgs<T>& a, cudaStream_t s) {
-    static size_t attr = 0;
-    if (a.smem > 48 * 1024 && a.smem > attr) {
+    if (a.smem > 48 * 1024) {  // per device, so set on every launch (host-side, cheap)
         cudaError_t e = cudaFuncSetAttribute(k_tail<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem);
         if (e != cudaSuccess) return e;
-        attr = a.smem;
     }
     return launch_pdl(k_tail<T>, dim3(1), dim3(kTailThreads), a.smem, s, a);
 }
