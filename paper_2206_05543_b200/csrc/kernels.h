@@ -51,6 +51,12 @@ template <class T>
 cudaError_t launch_sweep(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, int shape, T sA,
                          T sM, T omega, bool from_zero, cudaStream_t s, const NormOut* no = nullptr);
 bool sweep_fused_supported(int dim, int shape);
+// K1 + K2: xo = sweep(x) and bc = restrict(b - A xo) in one march (2D marching levels);
+// from_zero: x == 0; no != nullptr: the norm of the input residual is appended as well
+bool sweep_rr_supported(const Layout& L);
+template <class T>
+cudaError_t launch_sweep_rr(const Layout& L, const Layout& Lc, const T* x, const T* b, T* xo, T* bc, const Terms<T>& M,
+                            int shape, T sA, T sM, T omega, bool from_zero, cudaStream_t s, const NormOut* no);
 // K3 + K1: xo = sweep(x + P e) (prolongation + correction fused into the first post-sweep)
 bool sweep_pc_supported(const Layout& L);
 template <class T>

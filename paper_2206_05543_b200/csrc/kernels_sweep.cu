@@ -139,15 +139,6 @@ constexpr size_t m2_smem_bytes(bool pc = false) {
            + (size_t)M2_ST * 8;                             // mbarriers
 }
 
-// value of r row (o0 = -1, 0, +1 -> rm, rc, rp) at column v + o1 of this lane
-template <class T, int VEC>
-__device__ __forceinline__ T pick(const T* rm, const T* rc, const T* rp, T lm, T lc, T lp, T hm, T hc, T hp, int o0,
-                                  int o1, int v) {
-    const T* row = o0 < 0 ? rm : (o0 == 0 ? rc : rp);
-    if (o1 == 0) return row[v];
-    if (o1 < 0) return v > 0 ? row[v - 1] : (o0 < 0 ? lm : (o0 == 0 ? lc : lp));
-    return v + 1 < VEC ? row[v + 1] : (o0 < 0 ? hm : (o0 == 0 ? hc : hp));
-}
 
 template <class T>
 struct M2Ctx {

@@ -430,6 +430,7 @@ template <class T> struct Solver final : spaimg_solver {
     int shape = SHAPE_GENERIC;
     bool fused = false;      // fused K1 sweep available for this smoother
     bool fused_norm = false; // norm folded into the first pre-sweep (A) of the next cycle
+    bool a_rr = false;       // A also carries level 0's residual + restriction (K1+K2 march)
     bool k3_flip = false;    // (nu1+nu2) odd: the finest K3 writes the other buffer so a cycle ends in x[0]
     T omega{};
     T* lu = nullptr;
@@ -538,6 +539,7 @@ template <class T> struct Solver final : spaimg_solver {
         if (N != c.coarse_N || count_of(c.dim, N) != c.coarse_n)
             return fail(SPAIMG_EINVAL, "coarse factorisation does not match the coarsest level");
         fused_norm = nsmooth() >= 1 && c.nu1 >= 1 && fused && sweep_norm_supported();
+        a_rr = fused_norm && c.nu1 == 1 && sweep_rr_supported(lv[0].L);
         nlu = c.coarse_n;
         std::vector<T> luT(lu_h.begin(), lu_h.end());
         if (int rc = dalloc(&lu, luT.size())) return rc;
@@ -768,7 +770,7 @@ template <class T> struct Solver final : spaimg_solver {
     // recursive schedule (multigrid.py:157-185).  Returns the buffer index of level l holding
     // the result, or -1 on error.  pre_done: the first pre-sweep already ran (level 0: part A;
     // small levels: fused into the finer level's residual + restriction kernel).
-    int visit(int l, int a, bool fz, cudaStream_t s, int* launches, bool pre_done) {
+    int visit(int l, int a, bool fz, cudaStream_t s, int* launches, bool pre_done, bool rr_done = false) {
         if (l >= tail_l && l < nsmooth()) return tail_visit(l, a, fz, s, launches);
         Level<T>& L = lv[l];
         if (l == nsmooth()) {  // u.N <= coarsest_N: direct solve (multigrid.py:166-167)
@@ -776,9 +778,21 @@ template <class T> struct Solver final : spaimg_solver {
             ++*launches;
             return 0;
         }
+        Level<T>& C0 = lv[l + 1];
+        // the last pre-sweep of a 2D marching level carries the residual + restriction (K1+K2)
+        const bool pr = !rr_done && fused && cfg.nu1 >= 1 && sweep_rr_supported(L.L);
         for (int k = 0; k < cfg.nu1; ++k) {
-            if (!(pre_done && k == 0))
-                if (do_sweep<T>(L, a, fz, M, shape, fused, omega, s, launches)) return -1;
+            if (!(pre_done && k == 0)) {
+                if (pr && k == cfg.nu1 - 1) {
+                    if (launch_sweep_rr<T>(L.L, C0.L, L.x[a], L.b, L.x[1 - a], C0.b, M, shape, L.sA, L.sM, omega, fz, s,
+                                           nullptr) != cudaSuccess)
+                        return -1;
+                    ++*launches;
+                    rr_done = true;
+                } else if (do_sweep<T>(L, a, fz, M, shape, fused, omega, s, launches)) {
+                    return -1;
+                }
+            }
             a = 1 - a;
             fz = false;
         }
@@ -790,9 +804,11 @@ template <class T> struct Solver final : spaimg_solver {
         // on the small 2D levels the coarse level's first (zero-start) pre-sweep rides with K2
         // (measured: c2 -1.7 %, c1 -3.5 %; in 3D the ring recomputation costs more than the
         // launch it saves, c3 +7 %, so 3D keeps two kernels unless SPAIMG_RRFZ=1)
-        const bool rr_fz = fused && cfg.nu1 >= 1 && l + 1 < nsmooth() && l + 1 < tail_l &&
+        const bool rr_fz = !rr_done && fused && cfg.nu1 >= 1 && l + 1 < nsmooth() && l + 1 < tail_l &&
                            L.L.N <= flat_threshold(cfg.dim) && !getenv("SPAIMG_RESTRICT_V1") && rrfz_enabled(cfg.dim);
-        if (rr_fz) {
+        if (rr_done) {
+            // C.b came with the last pre-sweep
+        } else if (rr_fz) {
             if (launch_residual_restrict_fz<T>(L.L, C.L, L.x[a], L.b, C.b, C.x[1], M, shape, L.sA, C.sM, omega, s) !=
                 cudaSuccess)
                 return -1;
@@ -840,6 +856,12 @@ template <class T> struct Solver final : spaimg_solver {
         if (fused_norm) {
             Level<T>& L = lv[0];
             const NormOut no = fold_check ? norm_sink_cond(cur_cond) : norm_sink();
+            if (a_rr) {  // norm + first (only) pre-sweep + residual + restriction in one march
+                CK(launch_sweep_rr<T>(L.L, lv[1].L, L.x[0], L.b, L.x[1], lv[1].b, M, shape, L.sA, L.sM, omega, false, s,
+                                      &no));
+                ++*launches;
+                return 0;
+            }
             CK(launch_sweep<T>(L.L, L.x[0], L.b, L.x[1], M, shape, L.sA, L.sM, omega, false, s, &no));
             ++*launches;
             return 0;
@@ -849,7 +871,7 @@ template <class T> struct Solver final : spaimg_solver {
 
     // B: the rest of the cycle; ends with the iterate back in x[0]
     int part_b(cudaStream_t s, int* launches) {
-        const int out = visit(0, 0, false, s, launches, fused_norm);
+        const int out = visit(0, 0, false, s, launches, fused_norm, a_rr);
         if (out != 0) return fail(SPAIMG_EINVAL, out < 0 ? "cycle launch failed: " + g_err : "cycle parity error");
         return 0;
     }
