@@ -78,7 +78,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "25"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             time.sleep(0.25)
         except Exception:
             self.proc = None
@@ -423,10 +423,55 @@ def run_extras(sp, torch, stream, peak):
     except Exception as exc:  # extras never fail the headline line
         out["c4_error"] = repr(exc)
     try:
+        out["configs_1_4"] = config_sweep(sp, torch, stream, peak)
+    except Exception as exc:
+        out["configs_1_4_error"] = repr(exc)
+    try:
         out["config5"] = microbench(sp, torch, stream, peak)
     except Exception as exc:
         out["config5_error"] = repr(exc)
     return out
+
+
+def config_sweep(sp, torch, stream, peak):
+    """Every solve BASELINE.json configs 1-4 name (SPAI smoother vs weighted Jacobi, V(1,1) and
+    V(2,2), zero start, tol 1e-10): cycles, time to tolerance, per-cycle time, rho_hat and the
+    asymptotic per-cycle factor, with the V-cycle bytes-moved fraction."""
+    from paper_2206_05543_b200 import workloads
+    res = {}
+    for cfg_id in ("c1", "c2", "c3", "c4"):
+        dim, N, _ = workloads.CONFIGS[cfg_id]
+        bd = torch.as_tensor(workloads.rhs(cfg_id)).to("cuda")
+        spai = "m9" if dim == 2 else "m7"
+        jac = "jacobi2d" if dim == 2 else "jacobi3d"
+        runs = [(spai, 1), (spai, 2), (jac, 1), (jac, 2)] if cfg_id in ("c2", "c4") else [(spai, 1)]
+        for sm, nu in runs:
+            cfg = sp.MgConfig(smoother=sp.named(sm), cycle="V", nu1=nu, nu2=nu, coarsest_N=2, tol=1e-10)
+            so = sp.Solver(cfg, dim, N, device=torch.cuda.current_device())
+            so.load(bd)
+            so.run()
+            ts = []
+            for _ in range(3):
+                so.load(None)
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev0.record(stream)
+                hist, k, conv = so.run()
+                ev1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(ev0.elapsed_time(ev1) / 1e3)
+            t = float(np.median(ts))
+            st = so.stats()
+            rho = (hist[-1] / hist[0]) ** (1.0 / k) if k else None
+            res[f"{cfg_id}/{sm}/V({nu},{nu})"] = {
+                "cycles": k, "converged": conv, "time_to_tol_ms": t * 1e3, "ms_per_cycle": t / k * 1e3,
+                "dof_per_s": (N - 1) ** dim * k / t, "rho_hat": rho,
+                "last_cycle_factor": hist[-1] / hist[-2] if k >= 1 else None,
+                "vcycle_roofline_frac": st["bytes_per_cycle"] / (t / k) / 1e9 / peak}
+            del so
+        del bd
+        torch.cuda.empty_cache()
+    return res
 
 
 def microbench(sp, torch, stream, peak):
