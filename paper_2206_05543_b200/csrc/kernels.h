@@ -105,7 +105,7 @@ cudaError_t launch_coarse_solve(const Layout& L, const T* b, T* x, const T* lu, 
 // K5+: single-block, shared-memory-resident tail of the cycle (kernels_tail.cu): every level
 // from a threshold down runs inside one CTA, interpreting the host-recorded op list of the
 // recursion (levels relative to the entry level 0).
-enum TailOpType { TAIL_SWEEP = 0, TAIL_ZERO = 1, TAIL_RESTRICT = 2, TAIL_PROLONG = 3, TAIL_COARSE = 4 };
+enum TailOpType { TAIL_SWEEP = 0, TAIL_ZERO = 1, TAIL_RESTRICT = 2, TAIL_PROLONG = 3, TAIL_COARSE = 4, TAIL_SOLO = 5 };
 struct TailOp {
     int type;
     int level;        // index into the tail levels (0 = entry level)
@@ -142,5 +142,18 @@ template <class T> struct TailArgs {
     int entry_fz, entry_a, out_a;
 };
 template <class T> cudaError_t launch_tail(const TailArgs<T>& a, cudaStream_t s);
+// cluster tail (kernels_tail.cu): middle levels on a thread-block cluster over their global
+// buffers (ops with levels relative to the cluster entry level), TAIL_SOLO = the shared-memory
+// tail in CTA 0 for entry (a_in, fz)
+template <class T> struct ClusterArgs {
+    const TailLevel<T>* lv;  // device array: the cluster levels and the first solo level (global buffers)
+    const TailOp* ops;
+    int nops;
+    Terms<T> M;
+    T omega;
+    TailArgs<T> solo[2][2];
+};
+template <class T> cudaError_t launch_cluster_tail(const ClusterArgs<T>& a, int csize, size_t smem, cudaStream_t s);
+template <class T> cudaError_t cluster_occupancy(int csize, size_t smem, int* nclusters);
 
 }  // namespace spaimg

@@ -227,17 +227,21 @@ __device__ void tail_coarse_phase(const TailLevel<T>& v, T* y, const T* lu, cons
 }
 
 // copy the interior of one level between two layouts (global padded <-> shared compact)
-template <class T>
+template <class T, bool SRC_GLOBAL>
 __device__ void tail_copy(const Layout& Ld, T* dst, const Layout& Ls, const T* src) {
     const int cnt = npoints(Ld);
-    for (int q = threadIdx.x; q < cnt; q += blockDim.x) dst[tpoint(Ld, q)] = src[tpoint(Ls, q)];
+    for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+        // global sources through L2: in the cluster tail other CTAs of the cluster wrote them
+        if constexpr (SRC_GLOBAL) {
+            dst[tpoint(Ld, q)] = __ldcg(src + tpoint(Ls, q));
+        } else {
+            dst[tpoint(Ld, q)] = src[tpoint(Ls, q)];
+        }
+    }
 }
 
 template <class T>
-__global__ void __launch_bounds__(kTailThreads) k_tail(TailArgs<T> a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    pdl_wait();
-    pdl_trigger();
+__device__ void tail_body(const TailArgs<T>& a, unsigned char* smem_raw) {
     // [level descriptors | ops | level arrays | LU work vector y]
     TailLevel<T>* lv = reinterpret_cast<TailLevel<T>*>(smem_raw);
     TailOp* ops = reinterpret_cast<TailOp*>(lv + a.nlv);
@@ -254,8 +258,8 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(TailArgs<T> a) {
     for (int i = threadIdx.x; i < a.arr_elems; i += blockDim.x) arr[i] = T(0);
     __syncthreads();
     // entry level: b (and the start iterate) from its global buffers
-    tail_copy<T>(lv[0].L, lv[0].b, a.gL, a.gb);
-    if (!a.entry_fz) tail_copy<T>(lv[0].L, lv[0].x[a.entry_a], a.gL, a.gx_in);
+    tail_copy<T, true>(lv[0].L, lv[0].b, a.gL, a.gb);
+    if (!a.entry_fz) tail_copy<T, true>(lv[0].L, lv[0].x[a.entry_a], a.gL, a.gx_in);
     __syncthreads();
     for (int i = 0; i < a.nops; ++i) {
         const TailOp op = ops[i];
@@ -294,7 +298,216 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(TailArgs<T> a) {
         }
     }
     __syncthreads();
-    tail_copy<T>(a.gL, a.gx_out, lv[0].L, lv[0].x[a.out_a]);
+    tail_copy<T, false>(a.gL, a.gx_out, lv[0].L, lv[0].x[a.out_a]);
+}
+
+template <class T>
+__global__ void __launch_bounds__(kTailThreads) k_tail(TailArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_wait();
+    pdl_trigger();
+    tail_body<T>(a, smem_raw);
+}
+
+// ------------------------------------------------------------------------------------------
+// Cluster tail: the middle levels (above the shared-memory tail) run on a 16-CTA thread-block
+// cluster over their global (L2-resident) level buffers, point-parallel, phases separated by
+// hardware cluster barriers (barrier.cluster arrive.release / wait.acquire, ~0.7 us with an L2
+// round trip against several us per dependent kernel); the smallest levels then run as the
+// shared-memory tail in CTA 0 (TAIL_SOLO) while the other CTAs wait at the next barrier.
+// Cross-CTA data is read with ld.global.cg (L2).
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cluster_size() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+
+template <class T>
+__device__ __forceinline__ T cg_residual(const Layout& L, const T* x, const T* b, long long p, T sA) {
+    if (L.dim == 2)
+        return residual2d<T>(__ldcg(b + p), __ldcg(x + p), __ldcg(x + p + L.px), __ldcg(x + p - L.px), __ldcg(x + p + 1),
+                             __ldcg(x + p - 1), sA);
+    return residual3d<T>(__ldcg(b + p), __ldcg(x + p), __ldcg(x + p + L.pp), __ldcg(x + p - L.pp), __ldcg(x + p + L.px),
+                         __ldcg(x + p - L.px), __ldcg(x + p + 1), __ldcg(x + p - 1), sA);
+}
+
+template <class T>
+__device__ void cl_op(const ClusterArgs<T>& a, const TailOp& op, int start, int stride) {
+    using O = Op<T>;
+    const TailLevel<T>& v = a.lv[op.level];
+    const Layout& L = v.L;
+    const int cnt = npoints(L);
+    switch (op.type) {
+        case TAIL_SWEEP: {
+            for (int q = start; q < cnt; q += stride) {
+                const long long p = tpoint(L, q);
+                v.r[p] = op.fz ? __ldcg(v.b + p) : cg_residual<T>(L, v.x[op.a_in], v.b, p, v.sA);
+            }
+            cluster_sync_all();
+            const T* x = op.fz ? nullptr : v.x[op.a_in];
+            T* xo = v.x[op.a_out];
+            for (int q = start; q < cnt; q += stride) {
+                const long long p = tpoint(L, q);
+                T acc = T(0);
+                for (int k = 0; k < a.M.nt; ++k) {
+                    const long long o = L.dim == 2 ? (long long)a.M.off[k][0] * L.px + a.M.off[k][1]
+                                                   : (long long)a.M.off[k][0] * L.pp + (long long)a.M.off[k][1] * L.px +
+                                                         a.M.off[k][2];
+                    acc = O::add(acc, O::mul(a.M.c[k], __ldcg(v.r + p + o)));
+                }
+                xo[p] = relax<T>(x ? __ldcg(x + p) : T(0), acc, v.sM, a.omega);
+            }
+            break;
+        }
+        case TAIL_ZERO:
+            for (int q = start; q < cnt; q += stride) v.x[op.a_out][tpoint(L, q)] = T(0);
+            break;
+        case TAIL_RESTRICT: {
+            for (int q = start; q < cnt; q += stride) {
+                const long long p = tpoint(L, q);
+                v.r[p] = cg_residual<T>(L, v.x[op.a_in], v.b, p, v.sA);
+            }
+            cluster_sync_all();
+            const TailLevel<T>& c = a.lv[op.level + 1];
+            const Layout& Lc = c.L;
+            const int m = Lc.n;
+            const int cc = npoints(Lc);
+            const T* r = v.r;
+            for (int q = start; q < cc; q += stride) {
+                if (L.dim == 2) {
+                    const int I = q / m, K = q % m;
+                    T t[3];
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        const long long p = tidx(L, 2 * I + 1, 2 * K + k, 0);
+                        t[k] = fw<T>(__ldcg(r + p - L.px), __ldcg(r + p), __ldcg(r + p + L.px));
+                    }
+                    c.b[tidx(Lc, I, K, 0)] = fw<T>(t[0], t[1], t[2]);
+                } else {
+                    const int I = q / (m * m), J = (q / m) % m, K = q % m;
+                    T u[3];
+#pragma unroll
+                    for (int qk = 0; qk < 3; ++qk) {
+                        T t[3];
+#pragma unroll
+                        for (int qj = 0; qj < 3; ++qj) {
+                            const long long p = tidx(L, 2 * I + 1, 2 * J + qj, 2 * K + qk);
+                            t[qj] = fw<T>(__ldcg(r + p - L.pp), __ldcg(r + p), __ldcg(r + p + L.pp));
+                        }
+                        u[qk] = fw<T>(t[0], t[1], t[2]);
+                    }
+                    c.b[tidx(Lc, I, J, K)] = fw<T>(u[0], u[1], u[2]);
+                }
+            }
+            break;
+        }
+        case TAIL_PROLONG: {
+            const TailLevel<T>& c = a.lv[op.level + 1];
+            const Layout& Lc = c.L;
+            const int m = Lc.n, n = L.n;
+            const T* e = c.x[op.c];
+            const T* xi = v.x[op.a_in];
+            T* xo = v.x[op.a_out];
+            for (int q = start; q < cnt; q += stride) {
+                T val;
+                long long p;
+                if (L.dim == 2) {
+                    const int i0 = q / n, i1 = q % n;
+                    p = tidx(L, i0, i1, 0);
+                    auto t0 = [&](int j1) {
+                        return tail_interp<T>(i0, m, [&](int j0) { return __ldcg(e + tidx(Lc, j0, j1, 0)); });
+                    };
+                    val = tail_interp<T>(i1, m, t0);
+                } else {
+                    const int i0 = q / (n * n), i1 = (q / n) % n, i2 = q % n;
+                    p = tidx(L, i0, i1, i2);
+                    auto t1 = [&](int j2) {
+                        auto t0 = [&](int j1) {
+                            return tail_interp<T>(i0, m, [&](int j0) { return __ldcg(e + tidx(Lc, j0, j1, j2)); });
+                        };
+                        return tail_interp<T>(i1, m, t0);
+                    };
+                    val = tail_interp<T>(i2, m, t1);
+                }
+                xo[p] = O::add(__ldcg(xi + p), val);
+            }
+            break;
+        }
+        default:
+            break;
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kTailThreads) k_cluster_tail(ClusterArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_wait();
+    pdl_trigger();
+    const unsigned rank = cluster_rank();
+    const int start = (int)(rank * blockDim.x + threadIdx.x), stride = (int)(cluster_size() * blockDim.x);
+    for (int i = 0; i < a.nops; ++i) {
+        const TailOp op = a.ops[i];
+        if (i > 0) cluster_sync_all();
+        if (op.type == TAIL_SOLO) {
+            if (rank == 0) tail_body<T>(a.solo[op.a_in][op.fz], smem_raw);
+        } else {
+            cl_op<T>(a, op, start, stride);
+        }
+    }
+}
+
+template <class T>
+cudaError_t cluster_occupancy(int csize, size_t smem, int* nclusters) {
+    cudaError_t e = cudaFuncSetAttribute(k_cluster_tail<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    if (smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(k_cluster_tail<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(csize);
+    cfg.blockDim = dim3(kTailThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = csize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaOccupancyMaxActiveClusters(nclusters, k_cluster_tail<T>, &cfg);
+}
+
+template <class T>
+cudaError_t launch_cluster_tail(const ClusterArgs<T>& a, int csize, size_t smem, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(k_cluster_tail<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    if (smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(k_cluster_tail<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(csize);
+    cfg.blockDim = dim3(kTailThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = csize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_cluster_tail<T>, a);
 }
 
 template <class T>
@@ -308,5 +521,9 @@ cudaError_t launch_tail(const TailArgs<T>& a, cudaStream_t s) {
 
 template cudaError_t launch_tail<double>(const TailArgs<double>&, cudaStream_t);
 template cudaError_t launch_tail<float>(const TailArgs<float>&, cudaStream_t);
+template cudaError_t launch_cluster_tail<double>(const ClusterArgs<double>&, int, size_t, cudaStream_t);
+template cudaError_t cluster_occupancy<double>(int, size_t, int*);
+template cudaError_t cluster_occupancy<float>(int, size_t, int*);
+template cudaError_t launch_cluster_tail<float>(const ClusterArgs<float>&, int, size_t, cudaStream_t);
 
 }  // namespace spaimg

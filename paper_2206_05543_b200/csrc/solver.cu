@@ -527,7 +527,7 @@ template <class T> struct Solver final : spaimg_solver {
             if (int rc = dalloc(&l.b, (size_t)l.L.alloc)) return rc;
             if (!coarse) {
                 if (int rc = dalloc(&l.x[1], (size_t)l.L.alloc)) return rc;
-                if (!fused || getenv("SPAIMG_RESTRICT_V1") || N <= tail_threshold(c))  // scratch r
+                if (!fused || getenv("SPAIMG_RESTRICT_V1") || N <= std::max(tail_threshold(c), cluster_threshold(c)))
                     if (int rc = dalloc(&l.r, (size_t)l.L.alloc)) return rc;
             }
             lv.push_back(l);
@@ -547,6 +547,7 @@ template <class T> struct Solver final : spaimg_solver {
         if (int rc = dalloc(&piv, piv_h.size())) return rc;
         CK(cudaMemcpy(piv, piv_h.data(), piv_h.size() * sizeof(int), cudaMemcpyHostToDevice));
         if (int rc = init_tail()) return rc;
+        if (int rc = init_cluster()) return rc;
         norms_cap = 4097;
         if (int rc = dalloc(&norms_d, norms_cap)) return rc;
         if (int rc = dalloc(&slot_d, 1)) return rc;
@@ -720,10 +721,8 @@ template <class T> struct Solver final : spaimg_solver {
         return a;
     }
 
-    int tail_visit(int l, int a, bool fz, cudaStream_t s, int* launches) {
-        if (l != tail_l) return -1;
-        const int z = fz ? 1 : 0;
-        const Level<T>& G = lv[l];
+    TailArgs<T> make_tail_args(int a, int z) const {
+        const Level<T>& G = lv[tail_l];
         TailArgs<T> ta{};
         ta.lv = tail_lv;
         ta.ops = tail_ops[a][z];
@@ -744,9 +743,106 @@ template <class T> struct Solver final : spaimg_solver {
         ta.gx_out = G.x[ta.out_a];
         ta.entry_fz = z;
         ta.entry_a = a;
+        return ta;
+    }
+
+    int tail_visit(int l, int a, bool fz, cudaStream_t s, int* launches) {
+        if (l != tail_l) return -1;
+        const TailArgs<T> ta = make_tail_args(a, fz ? 1 : 0);
         if (launch_tail<T>(ta, s) != cudaSuccess) return -1;
         ++*launches;
         return ta.out_a;
+    }
+
+    // ---- cluster tail: levels cl_l .. tail_l-1 on a thread-block cluster, then the solo tail --
+    // opt-in (SPAIMG_CLUSTER_N): bitwise correct, but measured slower than the per-op kernels at
+    // every threshold (c1 +14 %, c2 +3 %, c3 2x at N<=64): point-parallel phases over L2 with a
+    // cluster barrier each lose to the shared-memory tiles of the flat kernels
+    static int cluster_threshold(const spaimg_mg_config&) {
+        const char* e = getenv("SPAIMG_CLUSTER_N");
+        return e ? atoi(e) : 0;
+    }
+    int cl_l = 1 << 30;
+    int cl_size = 16;
+    TailLevel<T>* cl_lv = nullptr;
+    TailOp* cl_ops[2][2] = {};
+    int cl_nops[2][2] = {};
+    int cl_out[2][2] = {};
+
+    int record_cluster(int l, int a, bool fz, std::vector<TailOp>& ops) {
+        const int rl = l - cl_l;
+        if (l == tail_l) {
+            ops.push_back(TailOp{TAIL_SOLO, rl, a, 0, 0, fz ? 1 : 0, 0, 0, 0, 0});
+            return tail_out[a][fz ? 1 : 0];
+        }
+        for (int k = 0; k < cfg.nu1; ++k) {
+            ops.push_back(TailOp{TAIL_SWEEP, rl, a, 1 - a, 0, fz ? 1 : 0, 0, 0, 0, 0});
+            a = 1 - a;
+            fz = false;
+        }
+        if (fz) ops.push_back(TailOp{TAIL_ZERO, rl, a, a, 0, 0, 0, 0, 0, 0});
+        ops.push_back(TailOp{TAIL_RESTRICT, rl, a, a, 0, 0, 0, 0, 0, 0});
+        int c = record_cluster(l + 1, 0, true, ops);
+        for (int g = 1; g < cfg.gamma; ++g) c = record_cluster(l + 1, c, false, ops);
+        ops.push_back(TailOp{TAIL_PROLONG, rl, a, a, c, 0, 0, 0, 0, 0});
+        for (int k = 0; k < cfg.nu2; ++k) {
+            ops.push_back(TailOp{TAIL_SWEEP, rl, a, 1 - a, 0, 0, 0, 0, 0, 0});
+            a = 1 - a;
+        }
+        return a;
+    }
+
+    int init_cluster() {
+        const int thr = cluster_threshold(cfg);
+        if (thr <= 0 || tail_l >= nsmooth() || !fused) return 0;
+        int l0 = tail_l;
+        while (l0 > 1 && lv[l0 - 1].L.N <= thr) --l0;
+        if (l0 >= tail_l) return 0;
+        // a 16-CTA cluster where the device allows one, else 8
+        {
+            int ncl = 0;
+            cl_size = cluster_occupancy<T>(16, tail_smem, &ncl) == cudaSuccess && ncl > 0 ? 16 : 8;
+        }
+        const int nt = tail_l + 1 - l0;
+        std::vector<TailLevel<T>> h(nt);
+        for (int i = 0; i < nt; ++i) {
+            const Level<T>& L = lv[l0 + i];
+            h[i].L = L.L;
+            h[i].x[0] = L.x[0];
+            h[i].x[1] = L.x[1];
+            h[i].b = L.b;
+            h[i].r = L.r;
+            h[i].sA = L.sA;
+            h[i].sM = L.sM;
+            if (i < nt - 1 && !L.r) return 0;  // needs the level's scratch r
+        }
+        if (int rc = dalloc(&cl_lv, (size_t)nt)) return rc;
+        CK(cudaMemcpy(cl_lv, h.data(), nt * sizeof(TailLevel<T>), cudaMemcpyHostToDevice));
+        cl_l = l0;
+        for (int a = 0; a < 2; ++a)
+            for (int fz = 0; fz < 2; ++fz) {
+                std::vector<TailOp> ops;
+                cl_out[a][fz] = record_cluster(l0, a, fz != 0, ops);
+                if (int rc = dalloc(&cl_ops[a][fz], ops.size())) return rc;
+                CK(cudaMemcpy(cl_ops[a][fz], ops.data(), ops.size() * sizeof(TailOp), cudaMemcpyHostToDevice));
+                cl_nops[a][fz] = (int)ops.size();
+            }
+        return 0;
+    }
+
+    int cluster_visit(int a, bool fz, cudaStream_t s, int* launches) {
+        const int z = fz ? 1 : 0;
+        ClusterArgs<T> ca{};
+        ca.lv = cl_lv;
+        ca.ops = cl_ops[a][z];
+        ca.nops = cl_nops[a][z];
+        ca.M = M;
+        ca.omega = omega;
+        for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j) ca.solo[i][j] = make_tail_args(i, j);
+        if (launch_cluster_tail<T>(ca, cl_size, tail_smem, s) != cudaSuccess) return -1;
+        ++*launches;
+        return cl_out[a][z];
     }
 
     // ||b - A x||_2 of the finest level appended to the device history
@@ -771,6 +867,7 @@ template <class T> struct Solver final : spaimg_solver {
     // the result, or -1 on error.  pre_done: the first pre-sweep already ran (level 0: part A;
     // small levels: fused into the finer level's residual + restriction kernel).
     int visit(int l, int a, bool fz, cudaStream_t s, int* launches, bool pre_done, bool rr_done = false) {
+        if (l == cl_l) return cluster_visit(a, fz, s, launches);
         if (l >= tail_l && l < nsmooth()) return tail_visit(l, a, fz, s, launches);
         Level<T>& L = lv[l];
         if (l == nsmooth()) {  // u.N <= coarsest_N: direct solve (multigrid.py:166-167)
@@ -804,7 +901,7 @@ template <class T> struct Solver final : spaimg_solver {
         // on the small 2D levels the coarse level's first (zero-start) pre-sweep rides with K2
         // (measured: c2 -1.7 %, c1 -3.5 %; in 3D the ring recomputation costs more than the
         // launch it saves, c3 +7 %, so 3D keeps two kernels unless SPAIMG_RRFZ=1)
-        const bool rr_fz = !rr_done && fused && cfg.nu1 >= 1 && l + 1 < nsmooth() && l + 1 < tail_l &&
+        const bool rr_fz = !rr_done && fused && cfg.nu1 >= 1 && l + 1 < nsmooth() && l + 1 < std::min(tail_l, cl_l) &&
                            L.L.N <= flat_threshold(cfg.dim) && !getenv("SPAIMG_RESTRICT_V1") && rrfz_enabled(cfg.dim);
         if (rr_done) {
             // C.b came with the last pre-sweep

@@ -256,7 +256,8 @@ def test_solve_batch_pipelined_matches_single_solves(dim, N, sm):
 @pytest.mark.parametrize("env", [{"SPAIMG_NO_GRAPH": "1"}, {"SPAIMG_RESTRICT_V1": "1"}, {"SPAIMG_SWEEP_V1": "1"},
                                  {"SPAIMG_PDL": "1"}, {"SPAIMG_PC_FLAT": "1"}, {"SPAIMG_TAIL_N": "0"},
                                  {"SPAIMG_FOLD_CHECK": "0"}, {"SPAIMG_SOLVE_IF": "1"}, {"SPAIMG_RRFZ": "0"}, {"SPAIMG_RRFZ": "1"},
-                                 {"SPAIMG_PR": "1"}, {"SPAIMG_PR": "1", "SPAIMG_FLAT_N2": "0"},
+                                 {"SPAIMG_PR": "1"}, {"SPAIMG_PR": "1", "SPAIMG_FLAT_N2": "0"}, {"SPAIMG_CLUSTER_N": "64"},
+                                 {"SPAIMG_CLUSTER_N": "1024"},
                                  {"SPAIMG_FLAT_N2": "0", "SPAIMG_FLAT_N3": "0", "SPAIMG_PC": "0"}],
                          ids=lambda e: ",".join(f"{k[7:]}={v}" for k, v in e.items()))
 def test_alternate_paths_bitwise(env):
