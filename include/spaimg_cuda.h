@@ -134,6 +134,14 @@ SPAIMG_API int spaimg_solver_cycles(spaimg_solver *s, int ncycles, void *stream)
 /* full solve loop on the loaded problem */
 SPAIMG_API int spaimg_solver_run(spaimg_solver *s, double tol, int max_iters, double *norms, int *iterations,
                       int *converged, void *stream);
+/* numpy Generator(PCG64).uniform(low, high, count) in C order into device memory, bitwise: the
+ * reference solve()'s random start default_rng(rng_seed).uniform(0, 1, shape) (multigrid.py:204-205)
+ * without a host draw or upload.  (state, inc) = the seeded generator's 128-bit PCG64 state
+ * (numpy: default_rng(seed).bit_generator.state), split into 64-bit halves. */
+SPAIMG_API int spaimg_fill_uniform(int dtype, long long count, unsigned long long state_hi,
+                                   unsigned long long state_lo, unsigned long long inc_hi, unsigned long long inc_lo,
+                                   double low, double high, void *out, void *stream);
+
 /* copy the current finest iterate out (dense layout) */
 SPAIMG_API int spaimg_solver_store(spaimg_solver *s, void *u_out, void *stream);
 /* nrhs independent zero-start solves of the solver's problem (solve() loop of multigrid.py:206-219

@@ -84,6 +84,8 @@ SIGNATURES = {
     "spaimg_solver_cycles": ([_VP, _I, _VP], _I),
     "spaimg_solver_run": ([_VP, _D, _I, _PD, _PI, _PI, _VP], _I),
     "spaimg_solver_store": ([_VP, _VP, _VP], _I),
+    "spaimg_fill_uniform": ([_I, ctypes.c_longlong, ctypes.c_ulonglong, ctypes.c_ulonglong, ctypes.c_ulonglong,
+                             ctypes.c_ulonglong, _D, _D, _VP, _VP], _I),
     "spaimg_solver_solve_batch": ([_VP, _I, ctypes.POINTER(_VP), ctypes.POINTER(_VP), _D, _I, _PD, _PI, _PI, _VP], _I),
     "spaimg_solver_op": ([_VP, _I, _I, _VP], _I),
 }

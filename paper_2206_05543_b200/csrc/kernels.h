@@ -102,6 +102,12 @@ template <class T>
 cudaError_t launch_coarse_solve(const Layout& L, const T* b, T* x, const T* lu, const int* piv, int nlu,
                                 cudaStream_t s);
 
+// numpy Generator(PCG64).uniform(low, high) draws in C order on the device, bitwise
+// (kernels_rng.cu); st = {state_hi, state_lo, inc_hi, inc_lo} of the seeded generator
+template <class T>
+cudaError_t launch_fill_uniform(T* out, long long count, const unsigned long long st[4], double low, double high,
+                                cudaStream_t s);
+
 // K5+: single-block, shared-memory-resident tail of the cycle (kernels_tail.cu): every level
 // from a threshold down runs inside one CTA, interpreting the host-recorded op list of the
 // recursion (levels relative to the entry level 0).

@@ -1422,6 +1422,19 @@ extern "C" int spaimg_solver_solve_batch(spaimg_solver* s, int nrhs, const void*
     return s->solve_batch(nrhs, b, u_out, tol, max_iters, norms, iterations, converged, (cudaStream_t)stream);
 }
 
+extern "C" int spaimg_fill_uniform(int dtype, long long count, unsigned long long state_hi,
+                                   unsigned long long state_lo, unsigned long long inc_hi, unsigned long long inc_lo,
+                                   double low, double high, void* out, void* stream) {
+    if (dtype != SPAIMG_F64 && dtype != SPAIMG_F32) return fail(SPAIMG_EINVAL, "dtype must be SPAIMG_F64 or SPAIMG_F32");
+    if (count < 0 || (count > 0 && !out)) return fail(SPAIMG_EINVAL, "bad output");
+    if (!is_device_ptr(out)) return fail(SPAIMG_EINVAL, "spaimg_fill_uniform writes device memory");
+    const unsigned long long st[4] = {state_hi, state_lo, inc_hi, inc_lo};
+    cudaStream_t s = (cudaStream_t)stream;
+    CK(dtype == SPAIMG_F64 ? launch_fill_uniform<double>(static_cast<double*>(out), count, st, low, high, s)
+                           : launch_fill_uniform<float>(static_cast<float*>(out), count, st, low, high, s));
+    return 0;
+}
+
 extern "C" int spaimg_solver_store(spaimg_solver* s, void* u_out, void* stream) {
     if (!s || !u_out) return fail(SPAIMG_EINVAL, "NULL argument");
     return s->store(u_out, (cudaStream_t)stream);

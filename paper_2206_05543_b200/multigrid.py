@@ -365,10 +365,26 @@ def _check_solve(b: Grid, cfg: MgConfig):
         raise ValueError(f"smoother dim {M.dim} != problem dim {b.dim}")
 
 
+def device_uniform(seed, like, low=0.0, high=1.0):
+    """np.random.default_rng(seed).uniform(low, high, like.shape) drawn on like's device (bitwise;
+    the host only runs numpy's seeding)."""
+    import torch
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    out = torch.empty(tuple(like.shape), dtype=like.dtype, device=like.device)
+    mask = (1 << 64) - 1
+    lib = _lib.load()
+    _lib.check(lib.spaimg_fill_uniform(_dtype_code(out), out.numel(), s >> 64, s & mask, inc >> 64, inc & mask,
+                                       float(low), float(high), out.data_ptr(), _stream_for(out)))
+    return out
+
+
 def _start_values(b: Grid, cfg: MgConfig, u0):
     """The start iterate: the reference's seeded U(0,1) draw (multigrid.py:204-205) when
     u0 is None; None (zero start, no upload) when u0 is 0; else the given values."""
     if u0 is None:
+        if is_device_array(b.values):  # drawn on the device, bitwise the numpy draw
+            return device_uniform(cfg.rng_seed, b.values, 0.0, 1.0)
         rng = np.random.default_rng(cfg.rng_seed)
         return _same_side(b.values, rng.uniform(0.0, 1.0, size=tuple(b.values.shape)))
     if isinstance(u0, (int, float)) and u0 == 0:

@@ -90,14 +90,17 @@ def test_cycles_vs_reference_golden(golden_ops, side):
     assert n >= 10
 
 
-def test_default_solve_vs_reference_golden(golden_meta):
-    """solve() with the reference's seeded U(0,1) start (multigrid.py:204-205)."""
+@pytest.mark.parametrize("side", ["host", "device"])
+def test_default_solve_vs_reference_golden(golden_meta, side):
+    """solve() with the reference's seeded U(0,1) start (multigrid.py:204-205); device grids draw
+    it on the GPU (spaimg_fill_uniform), host grids with numpy."""
     for key, rec in golden_meta["solves"].items():
         dim, N = rec["dim"], rec["N"]
         b = np.random.default_rng(rec["b_seed"]).uniform(-1, 1, (N - 1,) * dim)
         cfg = sp.MgConfig(smoother=sp.named(rec["smoother"]), cycle=rec["cycle"], nu1=rec["nu1"], nu2=rec["nu2"],
                           coarsest_N=rec["coarsest_N"], rng_seed=rec["rng_seed"])
-        u, rep = sp.solve(sp.Grid(N, b), cfg)
+        u, rep = sp.solve(sp.Grid(N, b if side == "host" else dev(b)), cfg)
+        u = sp.Grid(N, host(u))
         assert rep.iterations == rec["iterations"] and rep.converged == rec["converged"], key
         rel = max(abs(a - r) / r for a, r in zip(rep.residual_norms, rec["norms"]))
         assert rel < 1e-8, (key, rel)
@@ -302,3 +305,17 @@ def test_fp32_cycles_vs_oracle(dim, N, sm):
     ref = c_oracle.cycle(x, b, N, npo.terms_of(M.stencil), M.omega_opt_analytic, 1, 1, 1, 2, dtype=np.float32)
     assert got.dtype == np.float32
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("seed,shape,dtype", [(0, (4095, 4095), torch.float64), (1, (127, 127, 127), torch.float64),
+                                              (12345, (17, 33), torch.float32), (7, (1,), torch.float64)])
+def test_device_uniform_is_numpy_bitwise(seed, shape, dtype):
+    """The device PCG64 uniform draw equals numpy's default_rng(seed).uniform(0, 1, shape) bit for
+    bit (fp32: the float64 draw rounded once)."""
+    from paper_2206_05543_b200.multigrid import device_uniform
+    like = torch.empty(shape, dtype=dtype, device="cuda")
+    got = device_uniform(seed, like).cpu().numpy()
+    ref = np.random.default_rng(seed).uniform(0.0, 1.0, shape)
+    assert np.array_equal(got, ref.astype(got.dtype))
+    got2 = device_uniform(seed, like, -1.0, 1.0).cpu().numpy()
+    assert np.array_equal(got2, np.random.default_rng(seed).uniform(-1.0, 1.0, shape).astype(got2.dtype))
