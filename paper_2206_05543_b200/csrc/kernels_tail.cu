@@ -25,22 +25,44 @@ namespace spaimg {
 
 constexpr int kTailThreads = 1024;
 
-__device__ __forceinline__ long long tidx(const Layout& L, int i0, int i1, int i2) {
-    return L.origin + (long long)i0 * (L.dim == 2 ? L.px : L.pp) + (L.dim == 2 ? (long long)i1 : (long long)i1 * L.px + i2);
+// Tail levels are small (they fit one CTA's shared memory), so indices are 32-bit and the
+// point -> (i0, i1[, i2]) split uses one approximate reciprocal instead of the integer division
+// sequence (the largest stall source of the tail in the ncu source view).  tdiv(q, d) is exact
+// for the tail's sizes: (q + 0.5)/d lies at least 0.5/d from an integer, and __fdividef's error
+// (2 ulp of a quotient below n) stays under that for n*d < 2^20 (2D: n < 1024; 3D: n < 101).
+__device__ __forceinline__ int tdiv(int q, int d) { return __float2int_rz(__fdividef((float)q + 0.5f, (float)d)); }
+
+__device__ __forceinline__ int tidx(const Layout& L, int i0, int i1, int i2) {
+    return (int)L.origin + i0 * (int)(L.dim == 2 ? L.px : L.pp) + (L.dim == 2 ? i1 : i1 * (int)L.px + i2);
 }
 
-// interior point q (C order) -> padded index
-__device__ __forceinline__ long long tpoint(const Layout& L, int q) {
+// exact 64-bit versions for the cluster tail, whose levels live in global memory at any size
+__device__ __forceinline__ long long gidx(const Layout& L, int i0, int i1, int i2) {
+    return L.origin + (long long)i0 * (L.dim == 2 ? L.px : L.pp) + (L.dim == 2 ? (long long)i1 : (long long)i1 * L.px + i2);
+}
+__device__ __forceinline__ long long gpoint(const Layout& L, int q) {
     const int n = L.n;
     if (L.dim == 2) return L.origin + (long long)(q / n) * L.px + (q % n);
     const int i0 = q / (n * n), rem = q - i0 * n * n;
     return L.origin + (long long)i0 * L.pp + (long long)(rem / n) * L.px + (rem % n);
 }
 
+// interior point q (C order) -> padded index
+__device__ __forceinline__ int tpoint(const Layout& L, int q) {
+    const int n = L.n;
+    if (L.dim == 2) {
+        const int i0 = tdiv(q, n);
+        return (int)L.origin + i0 * (int)L.px + (q - i0 * n);
+    }
+    const int i0 = tdiv(q, n * n), rem = q - i0 * n * n;
+    const int i1 = tdiv(rem, n);
+    return (int)L.origin + i0 * (int)L.pp + i1 * (int)L.px + (rem - i1 * n);
+}
+
 __device__ __forceinline__ int npoints(const Layout& L) { return L.dim == 2 ? L.n * L.n : L.n * L.n * L.n; }
 
 template <class T>
-__device__ __forceinline__ T tail_residual(const Layout& L, const T* x, const T* b, long long p, T sA) {
+__device__ __forceinline__ T tail_residual(const Layout& L, const T* x, const T* b, int p, T sA) {
     if (L.dim == 2) return residual2d<T>(b[p], x[p], x[p + L.px], x[p - L.px], x[p + 1], x[p - 1], sA);
     return residual3d<T>(b[p], x[p], x[p + L.pp], x[p - L.pp], x[p + L.px], x[p - L.px], x[p + 1], x[p - 1], sA);
 }
@@ -51,7 +73,7 @@ __device__ void tail_residual_phase(const TailLevel<T>& v, const T* x, bool fz) 
     const Layout& L = v.L;
     const int cnt = npoints(L);
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
-        const long long p = tpoint(L, q);
+        const int p = tpoint(L, q);
         v.r[p] = fz ? v.b[p] : tail_residual<T>(L, x, v.b, p, v.sA);
     }
 }
@@ -63,11 +85,11 @@ __device__ void tail_relax_phase(const TailLevel<T>& v, const T* x, T* xo, const
     const Layout& L = v.L;
     const int cnt = npoints(L);
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
-        const long long p = tpoint(L, q);
+        const int p = tpoint(L, q);
         T acc = T(0);
         for (int k = 0; k < M.nt; ++k) {
-            const long long o = L.dim == 2 ? (long long)M.off[k][0] * L.px + M.off[k][1]
-                                           : (long long)M.off[k][0] * L.pp + (long long)M.off[k][1] * L.px + M.off[k][2];
+            const int o = L.dim == 2 ? M.off[k][0] * (int)L.px + M.off[k][1]
+                                     : M.off[k][0] * (int)L.pp + M.off[k][1] * (int)L.px + M.off[k][2];
             acc = O::add(acc, O::mul(M.c[k], v.r[p + o]));
         }
         xo[p] = relax<T>(x ? x[p] : T(0), acc, v.sM, omega);
@@ -84,23 +106,23 @@ __device__ void tail_restrict_phase(const TailLevel<T>& f, const TailLevel<T>& c
     const T* r = f.r;
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
         if (Lf.dim == 2) {
-            const int I = q / m, K = q % m;
+            const int I = tdiv(q, m), K = q - I * m;
             T t[3];
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                const long long p = tidx(Lf, 2 * I + 1, 2 * K + a, 0);
+                const int p = tidx(Lf, 2 * I + 1, 2 * K + a, 0);
                 t[a] = fw<T>(r[p - Lf.px], r[p], r[p + Lf.px]);
             }
             c.b[tidx(Lc, I, K, 0)] = fw<T>(t[0], t[1], t[2]);
         } else {
-            const int I = q / (m * m), J = (q / m) % m, K = q % m;
+            const int I = tdiv(q, m * m), rem = q - I * m * m, J = tdiv(rem, m), K = rem - J * m;
             T u[3];
 #pragma unroll
             for (int qk = 0; qk < 3; ++qk) {
                 T t[3];
 #pragma unroll
                 for (int qj = 0; qj < 3; ++qj) {
-                    const long long p = tidx(Lf, 2 * I + 1, 2 * J + qj, 2 * K + qk);
+                    const int p = tidx(Lf, 2 * I + 1, 2 * J + qj, 2 * K + qk);
                     t[qj] = fw<T>(r[p - Lf.pp], r[p], r[p + Lf.pp]);
                 }
                 u[qk] = fw<T>(t[0], t[1], t[2]);
@@ -130,15 +152,15 @@ __device__ void tail_prolong_phase(const TailLevel<T>& f, const TailLevel<T>& c,
     const int n = Lf.n;
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
         T val;
-        long long p;
+        int p;
         if (Lf.dim == 2) {
-            const int i0 = q / n, i1 = q % n;
+            const int i0 = tdiv(q, n), i1 = q - i0 * n;
             p = tidx(Lf, i0, i1, 0);
             // axis 0 at fine row i0 for coarse column j1, then axis 1
             auto t0 = [&](int j1) { return tail_interp<T>(i0, m, [&](int j0) { return e[tidx(Lc, j0, j1, 0)]; }); };
             val = tail_interp<T>(i1, m, t0);
         } else {
-            const int i0 = q / (n * n), i1 = (q / n) % n, i2 = q % n;
+            const int i0 = tdiv(q, n * n), rem = q - i0 * n * n, i1 = tdiv(rem, n), i2 = rem - i1 * n;
             p = tidx(Lf, i0, i1, i2);
             auto t1 = [&](int j2) {
                 auto t0 = [&](int j1) {
@@ -349,14 +371,14 @@ __device__ void cl_op(const ClusterArgs<T>& a, const TailOp& op, int start, int 
     switch (op.type) {
         case TAIL_SWEEP: {
             for (int q = start; q < cnt; q += stride) {
-                const long long p = tpoint(L, q);
+                const long long p = gpoint(L, q);
                 v.r[p] = op.fz ? __ldcg(v.b + p) : cg_residual<T>(L, v.x[op.a_in], v.b, p, v.sA);
             }
             cluster_sync_all();
             const T* x = op.fz ? nullptr : v.x[op.a_in];
             T* xo = v.x[op.a_out];
             for (int q = start; q < cnt; q += stride) {
-                const long long p = tpoint(L, q);
+                const long long p = gpoint(L, q);
                 T acc = T(0);
                 for (int k = 0; k < a.M.nt; ++k) {
                     const long long o = L.dim == 2 ? (long long)a.M.off[k][0] * L.px + a.M.off[k][1]
@@ -369,11 +391,11 @@ __device__ void cl_op(const ClusterArgs<T>& a, const TailOp& op, int start, int 
             break;
         }
         case TAIL_ZERO:
-            for (int q = start; q < cnt; q += stride) v.x[op.a_out][tpoint(L, q)] = T(0);
+            for (int q = start; q < cnt; q += stride) v.x[op.a_out][gpoint(L, q)] = T(0);
             break;
         case TAIL_RESTRICT: {
             for (int q = start; q < cnt; q += stride) {
-                const long long p = tpoint(L, q);
+                const long long p = gpoint(L, q);
                 v.r[p] = cg_residual<T>(L, v.x[op.a_in], v.b, p, v.sA);
             }
             cluster_sync_all();
@@ -384,28 +406,28 @@ __device__ void cl_op(const ClusterArgs<T>& a, const TailOp& op, int start, int 
             const T* r = v.r;
             for (int q = start; q < cc; q += stride) {
                 if (L.dim == 2) {
-                    const int I = q / m, K = q % m;
+                    const int I = tdiv(q, m), K = q - I * m;
                     T t[3];
 #pragma unroll
                     for (int k = 0; k < 3; ++k) {
-                        const long long p = tidx(L, 2 * I + 1, 2 * K + k, 0);
+                        const long long p = gidx(L, 2 * I + 1, 2 * K + k, 0);
                         t[k] = fw<T>(__ldcg(r + p - L.px), __ldcg(r + p), __ldcg(r + p + L.px));
                     }
-                    c.b[tidx(Lc, I, K, 0)] = fw<T>(t[0], t[1], t[2]);
+                    c.b[gidx(Lc, I, K, 0)] = fw<T>(t[0], t[1], t[2]);
                 } else {
-                    const int I = q / (m * m), J = (q / m) % m, K = q % m;
+                    const int I = tdiv(q, m * m), rem = q - I * m * m, J = tdiv(rem, m), K = rem - J * m;
                     T u[3];
 #pragma unroll
                     for (int qk = 0; qk < 3; ++qk) {
                         T t[3];
 #pragma unroll
                         for (int qj = 0; qj < 3; ++qj) {
-                            const long long p = tidx(L, 2 * I + 1, 2 * J + qj, 2 * K + qk);
+                            const long long p = gidx(L, 2 * I + 1, 2 * J + qj, 2 * K + qk);
                             t[qj] = fw<T>(__ldcg(r + p - L.pp), __ldcg(r + p), __ldcg(r + p + L.pp));
                         }
                         u[qk] = fw<T>(t[0], t[1], t[2]);
                     }
-                    c.b[tidx(Lc, I, J, K)] = fw<T>(u[0], u[1], u[2]);
+                    c.b[gidx(Lc, I, J, K)] = fw<T>(u[0], u[1], u[2]);
                 }
             }
             break;
@@ -422,17 +444,17 @@ __device__ void cl_op(const ClusterArgs<T>& a, const TailOp& op, int start, int 
                 long long p;
                 if (L.dim == 2) {
                     const int i0 = q / n, i1 = q % n;
-                    p = tidx(L, i0, i1, 0);
+                    p = gidx(L, i0, i1, 0);
                     auto t0 = [&](int j1) {
-                        return tail_interp<T>(i0, m, [&](int j0) { return __ldcg(e + tidx(Lc, j0, j1, 0)); });
+                        return tail_interp<T>(i0, m, [&](int j0) { return __ldcg(e + gidx(Lc, j0, j1, 0)); });
                     };
                     val = tail_interp<T>(i1, m, t0);
                 } else {
-                    const int i0 = q / (n * n), i1 = (q / n) % n, i2 = q % n;
-                    p = tidx(L, i0, i1, i2);
+                    const int i0 = tdiv(q, n * n), rem = q - i0 * n * n, i1 = tdiv(rem, n), i2 = rem - i1 * n;
+                    p = gidx(L, i0, i1, i2);
                     auto t1 = [&](int j2) {
                         auto t0 = [&](int j1) {
-                            return tail_interp<T>(i0, m, [&](int j0) { return __ldcg(e + tidx(Lc, j0, j1, j2)); });
+                            return tail_interp<T>(i0, m, [&](int j0) { return __ldcg(e + gidx(Lc, j0, j1, j2)); });
                         };
                         return tail_interp<T>(i1, m, t0);
                     };

@@ -23,7 +23,10 @@ x = torch.as_tensor(rng.uniform(-1, 1, shape)).cuda()
 b = torch.as_tensor(rng.uniform(-1, 1, shape)).cuda()
 if dtype == "float32":
     x, b = x.float(), b.float()
-cfg = sp.MgConfig(smoother=sp.named(sm), cycle="V", nu1=1, nu2=1, coarsest_N=2)
+# CYCLE=W NU1=1 NU2=0 CN=4 selects the reference MgConfig defaults instead of V(1,1), cN=2
+env = os.environ.get
+cfg = sp.MgConfig(smoother=sp.named(sm), cycle=env("CYCLE", "V"), nu1=int(env("NU1", 1)), nu2=int(env("NU2", 1)),
+                  coarsest_N=int(env("CN", 2)))
 s = sp.Solver(cfg, dim, N, dtype=dtype)
 s.load(b, x)
 if op == 9:

@@ -1,5 +1,7 @@
-"""W-cycle (reference MgConfig defaults: W(1,0), coarsest_N=4) per-cycle time vs SPAIMG_TAIL_N.
-    python tools/tune_w.py c2 32,64,128"""
+"""W-cycle (reference MgConfig defaults: W(1,0), coarsest_N=4) per-cycle time vs SPAIMG_TAIL_N
+(or another SPAIMG_* switch).
+    python tools/tune_w.py c2 32,64,128
+    python tools/tune_w.py c2 SPAIMG_CLUSTER_N=0,64,256"""
 import os
 import sys
 
@@ -15,9 +17,10 @@ dim, N, _ = workloads.CONFIGS[cid]
 sm = "m9" if dim == 2 else "m7"
 b = torch.as_tensor(workloads.rhs(cid)).cuda()
 cfg = sp.MgConfig(smoother=sp.named(sm))  # reference defaults: cycle="W", nu1=1, nu2=0, coarsest_N=4
+var, vals = sys.argv[2].split("=", 1) if "=" in sys.argv[2] else ("SPAIMG_TAIL_N", sys.argv[2])
 ref = None
-for t in sys.argv[2].split(","):
-    os.environ["SPAIMG_TAIL_N"] = t
+for t in vals.split(","):
+    os.environ[var] = t
     s = sp.Solver(cfg, dim, N)
     s.load(b)
     ts = []
@@ -31,6 +34,6 @@ for t in sys.argv[2].split(","):
         ts.append(e0.elapsed_time(e1) / k)
     same = "ref" if ref is None else ("same" if h == ref else "DIFF")
     ref = ref or h
-    print(f"{cid} {sm} W(1,0) cN=4 tail={t}: {np.median(ts[1:]):.3f} ms/cycle, {k} cycles, "
+    print(f"{cid} {sm} W(1,0) cN=4 {var}={t}: {np.median(ts[1:]):.3f} ms/cycle, {k} cycles, "
           f"{s.stats()['kernels_per_cycle']} kernels/cycle, {same}", flush=True)
     del s
