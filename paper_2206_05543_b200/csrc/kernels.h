@@ -146,6 +146,7 @@ template <class T> struct TailArgs {
     const T* gx_in;          // start iterate (entry_fz == 0)
     T* gx_out;               // result iterate
     int entry_fz, entry_a, out_a;
+    int shape;               // SHAPE_* of M: named shapes get a compile-time term loop
 };
 template <class T> cudaError_t launch_tail(const TailArgs<T>& a, cudaStream_t s);
 // cluster tail (kernels_tail.cu): middle levels on a thread-block cluster over their global

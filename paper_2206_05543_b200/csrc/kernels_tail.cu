@@ -78,19 +78,35 @@ __device__ void tail_residual_phase(const TailLevel<T>& v, const T* x, bool fz) 
     }
 }
 
-// xo = x + omega * ((M r) * sM)   (x == nullptr: from zero)
-template <class T>
+// xo = x + omega * ((M r) * sM)   (x == nullptr: from zero).  Named shapes (S != GENERIC) unroll
+// the term loop with compile-time offsets, so every r load of a point issues at once.
+template <class T, int S>
 __device__ void tail_relax_phase(const TailLevel<T>& v, const T* x, T* xo, const Terms<T>& M, T omega) {
     using O = Op<T>;
     const Layout& L = v.L;
     const int cnt = npoints(L);
+    const int px = (int)L.px, pp = (int)L.pp;
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
         const int p = tpoint(L, q);
         T acc = T(0);
-        for (int k = 0; k < M.nt; ++k) {
-            const int o = L.dim == 2 ? M.off[k][0] * (int)L.px + M.off[k][1]
-                                     : M.off[k][0] * (int)L.pp + M.off[k][1] * (int)L.px + M.off[k][2];
-            acc = O::add(acc, O::mul(M.c[k], v.r[p + o]));
+        if constexpr (S == SHAPE_GENERIC) {
+            for (int k = 0; k < M.nt; ++k) {
+                const int o = L.dim == 2 ? M.off[k][0] * px + M.off[k][1]
+                                         : M.off[k][0] * pp + M.off[k][1] * px + M.off[k][2];
+                acc = O::add(acc, O::mul(M.c[k], v.r[p + o]));
+            }
+        } else {
+            constexpr int NT = ShapeT<S>::nt;
+            constexpr bool D3 = S == SHAPE_STAR7;
+            T rv[NT];
+#pragma unroll
+            for (int k = 0; k < NT; ++k) {
+                const int o = D3 ? ShapeT<S>::o(k, 0) * pp + ShapeT<S>::o(k, 1) * px + ShapeT<S>::o(k, 2)
+                                 : ShapeT<S>::o(k, 0) * px + ShapeT<S>::o(k, 1);
+                rv[k] = v.r[p + o];
+            }
+#pragma unroll
+            for (int k = 0; k < NT; ++k) acc = O::add(acc, O::mul(M.c[k], rv[k]));
         }
         xo[p] = relax<T>(x ? x[p] : T(0), acc, v.sM, omega);
     }
@@ -262,7 +278,7 @@ __device__ void tail_copy(const Layout& Ld, T* dst, const Layout& Ls, const T* s
     }
 }
 
-template <class T>
+template <class T, int S>
 __device__ void tail_body(const TailArgs<T>& a, unsigned char* smem_raw) {
     // [level descriptors | ops | level arrays | LU work vector y]
     TailLevel<T>* lv = reinterpret_cast<TailLevel<T>*>(smem_raw);
@@ -294,7 +310,7 @@ __device__ void tail_body(const TailArgs<T>& a, unsigned char* smem_raw) {
             case TAIL_SWEEP:
                 tail_residual_phase<T>(v, v.x[op.a_in], op.fz);
                 tbar(op.bid_in, op.nthr);
-                tail_relax_phase<T>(v, op.fz ? nullptr : v.x[op.a_in], v.x[op.a_out], a.M, a.omega);
+                tail_relax_phase<T, S>(v, op.fz ? nullptr : v.x[op.a_in], v.x[op.a_out], a.M, a.omega);
                 break;
             case TAIL_ZERO: {
                 const int cnt = npoints(v.L);
@@ -323,12 +339,12 @@ __device__ void tail_body(const TailArgs<T>& a, unsigned char* smem_raw) {
     tail_copy<T, false>(a.gL, a.gx_out, lv[0].L, lv[0].x[a.out_a]);
 }
 
-template <class T>
+template <class T, int S>
 __global__ void __launch_bounds__(kTailThreads) k_tail(TailArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_wait();
     pdl_trigger();
-    tail_body<T>(a, smem_raw);
+    tail_body<T, S>(a, smem_raw);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -480,7 +496,7 @@ __global__ void __launch_bounds__(kTailThreads) k_cluster_tail(ClusterArgs<T> a)
         const TailOp op = a.ops[i];
         if (i > 0) cluster_sync_all();
         if (op.type == TAIL_SOLO) {
-            if (rank == 0) tail_body<T>(a.solo[op.a_in][op.fz], smem_raw);
+            if (rank == 0) tail_body<T, SHAPE_GENERIC>(a.solo[op.a_in][op.fz], smem_raw);
         } else {
             cl_op<T>(a, op, start, stride);
         }
@@ -532,13 +548,32 @@ cudaError_t launch_cluster_tail(const ClusterArgs<T>& a, int csize, size_t smem,
     return cudaLaunchKernelEx(&cfg, k_cluster_tail<T>, a);
 }
 
-template <class T>
-cudaError_t launch_tail(const TailArgs<T>& a, cudaStream_t s) {
+template <class T, int S>
+static cudaError_t launch_tail_s(const TailArgs<T>& a, cudaStream_t s) {
     if (a.smem > 48 * 1024) {  // per device, so set on every launch (host-side, cheap)
-        cudaError_t e = cudaFuncSetAttribute(k_tail<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem);
+        cudaError_t e = cudaFuncSetAttribute(k_tail<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem);
         if (e != cudaSuccess) return e;
     }
-    return launch_pdl(k_tail<T>, dim3(1), dim3(kTailThreads), a.smem, s, a);
+    return launch_pdl(k_tail<T, S>, dim3(1), dim3(kTailThreads), a.smem, s, a);
+}
+
+template <class T>
+cudaError_t launch_tail(const TailArgs<T>& a, cudaStream_t s) {
+    const int dim = a.gL.dim;
+    switch (a.shape) {
+        case SHAPE_C1: return launch_tail_s<T, SHAPE_C1>(a, s);
+        case SHAPE_STAR5:
+            if (dim == 2) return launch_tail_s<T, SHAPE_STAR5>(a, s);
+            break;
+        case SHAPE_BOX9:
+            if (dim == 2) return launch_tail_s<T, SHAPE_BOX9>(a, s);
+            break;
+        case SHAPE_STAR7:
+            if (dim == 3) return launch_tail_s<T, SHAPE_STAR7>(a, s);
+            break;
+        default: break;
+    }
+    return launch_tail_s<T, SHAPE_GENERIC>(a, s);
 }
 
 template cudaError_t launch_tail<double>(const TailArgs<double>&, cudaStream_t);

@@ -742,6 +742,7 @@ template <class T> struct Solver final : spaimg_solver {
         ta.out_a = tail_out[a][z];
         ta.gx_out = G.x[ta.out_a];
         ta.entry_fz = z;
+        ta.shape = shape;
         ta.entry_a = a;
         return ta;
     }
