@@ -7,21 +7,15 @@
 
 namespace spaimg {
 
-// launch with the Programmatic-Dependent-Launch attribute when SPAIMG_PDL=1; the kernel
-// must call pdl_wait() before its first global memory access
-bool pdl_enabled();
+// typed kernel launch (arguments converted to the kernel's parameter types)
 template <class... KP, class... A>
-inline cudaError_t launch_pdl(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
+inline cudaError_t launch_k(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = 0;
     return cudaLaunchKernelEx(&cfg, k, static_cast<KP>(args)...);
 }
 
@@ -51,18 +45,11 @@ template <class T>
 cudaError_t launch_sweep(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, int shape, T sA,
                          T sM, T omega, bool from_zero, cudaStream_t s, const NormOut* no = nullptr);
 bool sweep_fused_supported(int dim, int shape);
-// K1 + K2: xo = sweep(x) and bc = restrict(b - A xo) in one march (2D marching levels);
-// from_zero: x == 0; no != nullptr: the norm of the input residual is appended as well
-bool sweep_rr_supported(const Layout& L);
-template <class T>
-cudaError_t launch_sweep_rr(const Layout& L, const Layout& Lc, const T* x, const T* b, T* xo, T* bc, const Terms<T>& M,
-                            int shape, T sA, T sM, T omega, bool from_zero, cudaStream_t s, const NormOut* no);
 // K3 + K1: xo = sweep(x + P e) (prolongation + correction fused into the first post-sweep)
 bool sweep_pc_supported(const Layout& L);
 template <class T>
 cudaError_t launch_sweep_pc(const Layout& L, const Layout& Lc, const T* x, const T* e, const T* b, T* xo,
                             const Terms<T>& M, int shape, T sA, T sM, T omega, cudaStream_t s);
-bool sweep_norm_supported();
 // K4 through the marching kernels: ||b - A x|| appended to the device history
 template <class T>
 cudaError_t launch_norm_march(const Layout& L, const T* x, const T* b, T sA, const NormOut& no, cudaStream_t s);
@@ -70,7 +57,7 @@ cudaError_t launch_norm_march(const Layout& L, const T* x, const T* b, T sA, con
 // K2: fused residual + full-weighting restriction
 template <class T>
 cudaError_t launch_residual_restrict(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T sA,
-                                     T* scratch_r, cudaStream_t s);
+                                     cudaStream_t s);
 // K2 / K1 for small levels: flat one-wave kernels (kernels_flat.cu); levels with mesh count
 // N <= flat_threshold(dim) use them instead of the marching kernels
 int flat_threshold(int dim);
@@ -79,9 +66,6 @@ int flat_threshold(int dim);
 template <class T>
 cudaError_t launch_residual_restrict_fz(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T* xc,
                                         const Terms<T>& M, int shape, T sA, T sMc, T omega, cudaStream_t s);
-template <class T>
-cudaError_t launch_sweep_pc_flat(const Layout& L, const Layout& Lc, const T* x, const T* e, const T* b, T* xo,
-                                 const Terms<T>& M, int shape, T sA, T sM, T omega, cudaStream_t s);
 template <class T>
 cudaError_t launch_residual_restrict_flat(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T sA,
                                           cudaStream_t s);
@@ -108,59 +92,62 @@ template <class T>
 cudaError_t launch_fill_uniform(T* out, long long count, const unsigned long long st[4], double low, double high,
                                 cudaStream_t s);
 
-// K5+: single-block, shared-memory-resident tail of the cycle (kernels_tail.cu): every level
-// from a threshold down runs inside one CTA, interpreting the host-recorded op list of the
-// recursion (levels relative to the entry level 0).
-enum TailOpType { TAIL_SWEEP = 0, TAIL_ZERO = 1, TAIL_RESTRICT = 2, TAIL_PROLONG = 3, TAIL_COARSE = 4, TAIL_SOLO = 5 };
-struct TailOp {
-    int type;
-    int level;        // index into the tail levels (0 = entry level)
-    int a_in, a_out;  // x buffer indices of the level
-    int c;            // PROLONG: x buffer of the coarse level holding the correction
-    int fz;           // SWEEP: the input iterate is zero (x not read)
-    int nthr;         // participating threads (a multiple of 32): the op's largest point count
-    int npre;         // threads meeting at the barrier before the op: max(nthr, previous op's nthr)
-    int bid_pre, bid_in;  // named-barrier ids for npre / nthr threads (0 = __syncthreads)
+// K5+: the shared-memory coarse-grid engine (kernels_tail.cu).  Every level from a size
+// threshold down lives in one CTA's shared memory; the CTA interprets the host-recorded op list
+// of the V/W recursion below its entry level (multigrid.py:157-185), each op point-parallel
+// over the op's level, ops separated by barriers over the warps involved.
+constexpr int kTailThreads = 512;
+enum TailOpType : int {
+    TAIL_RES = 0,      // r = b - A x                               (multigrid.py:99, :176)
+    TAIL_RELAX = 1,    // x = x + omega ((M r) sM), in place         (multigrid.py:100)
+    TAIL_RELAX0 = 2,   // x = 0 + omega ((M b) sM): first sweep from a zero iterate (r == b)
+    TAIL_ZERO = 3,     // x = 0 (nu1 == 0 on a zero start)
+    TAIL_FW = 4,       // coarse b = full weighting of r             (multigrid.py:104-119)
+    TAIL_PROLONG = 5,  // x = x + P (coarse x)                       (multigrid.py:122-144, :184)
+    TAIL_COARSE = 6,   // x = (LU)^-1 b in getrs order                (multigrid.py:147-154)
 };
-template <class T> struct TailLevel {
-    Layout L;   // compact shared-memory layout (frame = stencil radius)
-    T* x[2];    // host side: element offsets into the shared array block
-    T* b;
-    T* r;
-    T sA, sM;
+// One op (host-recorded).  Array offsets are element offsets, from the start of the level-array
+// block, of each array's interior point 0:
+//   RES: a0 = x, a1 = b, a2 = r, s = sA     RELAX: a0 = x, a2 = r, s = sM
+//   RELAX0: a0 = x, a1 = b, s = sM           ZERO: a0 = x
+//   FW: a2 = fine r, a1 = coarse b           PROLONG: a0 = fine x, a1 = coarse x
+//   COARSE: a0 = x, a1 = b
+template <class T> struct alignas(16) TailOp {
+    int type;
+    int logw;       // the level's points are mapped onto a W^dim box, W = 1 << logw
+    int nw;         // warps executing the op (a prefix of the CTA)
+    int bw;         // warps meeting at the barrier before the op: max(nw of this op and the previous)
+    int bid;        // barrier for bw warps: 0 = __syncthreads, -1 = __syncwarp, else a named barrier id
+    int n;          // interior points per axis
+    int s0, s1;     // element pitch of axis 0 and (3D) axis 1
+    int a0, a1, a2;
+    int m, cs0, cs1;  // FW / PROLONG: the coarse level's interior size and pitches
+    int pad;
+    T s;
 };
 template <class T> struct TailArgs {
-    const TailLevel<T>* lv;  // device array, nlv entries
-    const TailOp* ops;       // device array, nops entries
-    int nlv, nops;
-    size_t arr_off;          // byte offset of the level arrays in shared memory
-    int arr_elems;           // elements of all level arrays (y follows them)
+    const TailOp<T>* ops;    // device array, nops entries
+    int nops;
+    const T* coarse;         // [nlu*nlu: -LU off the diagonal, row-major | U_jj (nlu) | 1/U_jj (nlu)]
+    const int* coarse_idx;   // [nlu: b offset of row perm[i] | nlu: x offset of unknown i]
+    int nlu;
+    int coarse_off;          // byte offset of the coarse data in shared memory
+    int arr_off;             // byte offset of the level-array block in shared memory
+    int arr_elems;           // T elements of the level-array block
+    int zero_from;           // elements [zero_from, arr_elems) are zeroed on entry (level 0's r onwards)
     size_t smem;             // dynamic shared memory bytes
     Terms<T> M;
     T omega;
-    const T* lu;
-    const int* piv;
-    int nlu;
-    Layout gL;               // entry level in global memory
+    // the entry level: b and the start iterate come from its global buffers (zero frames
+    // included), the result goes back to gx (in place)
+    Layout gL;
     const T* gb;
-    const T* gx_in;          // start iterate (entry_fz == 0)
-    T* gx_out;               // result iterate
-    int entry_fz, entry_a, out_a;
-    int shape;               // SHAPE_* of M: named shapes get a compile-time term loop
+    T* gx;
+    int frame;               // F: zero frame width of the shared-memory arrays (stencil radius)
+    int e_s0, e_s1;          // shared-memory pitches of the entry level
+    int e_x, e_b;            // interior offsets of the entry level's x and b
+    int shape;               // SHAPE_* of M: named shapes get compile-time stencil offsets
 };
 template <class T> cudaError_t launch_tail(const TailArgs<T>& a, cudaStream_t s);
-// cluster tail (kernels_tail.cu): middle levels on a thread-block cluster over their global
-// buffers (ops with levels relative to the cluster entry level), TAIL_SOLO = the shared-memory
-// tail in CTA 0 for entry (a_in, fz)
-template <class T> struct ClusterArgs {
-    const TailLevel<T>* lv;  // device array: the cluster levels and the first solo level (global buffers)
-    const TailOp* ops;
-    int nops;
-    Terms<T> M;
-    T omega;
-    TailArgs<T> solo[2][2];
-};
-template <class T> cudaError_t launch_cluster_tail(const ClusterArgs<T>& a, int csize, size_t smem, cudaStream_t s);
-template <class T> cudaError_t cluster_occupancy(int csize, size_t smem, int* nclusters);
 
 }  // namespace spaimg

@@ -242,8 +242,6 @@ __global__ void __launch_bounds__(128) k_prolong_correct2d(Layout Lf, Layout Lc,
     using O = Op<T>;
     constexpr int C = 16 / (2 * (int)sizeof(T));
     constexpr int V = 2 * C;  // fine columns per thread
-    pdl_wait();
-    pdl_trigger();
     const int m = Lc.n;
     const int J0 = (blockIdx.x * blockDim.x + threadIdx.x) * C;
     const int I = blockIdx.y;
@@ -319,8 +317,6 @@ __global__ void __launch_bounds__(128) k_prolong_correct3d(Layout Lf, Layout Lc,
     using O = Op<T>;
     constexpr int C = 16 / (2 * (int)sizeof(T));
     constexpr int V = 2 * C;
-    pdl_wait();
-    pdl_trigger();
     const int m = Lc.n;
     const int K0 = (blockIdx.x * blockDim.x + threadIdx.x) * C;
     const int J = blockIdx.y, I = blockIdx.z;
@@ -406,11 +402,11 @@ cudaError_t launch_prolong_correct(const Layout& Lf, const Layout& Lc, const T* 
     if (Lf.dim == 2) {
         constexpr int C = 16 / (2 * (int)sizeof(T));
         dim3 g(((m + 1 + C - 1) / C + 127) / 128, m + 1);
-        return launch_pdl(k_prolong_correct2d<T>, g, dim3(128), 0, s, Lf, Lc, xi, xo, e, acc);
+        return launch_k(k_prolong_correct2d<T>, g, dim3(128), 0, s, Lf, Lc, xi, xo, e, acc);
     } else {
         constexpr int C = 16 / (2 * (int)sizeof(T));
         dim3 g(((m + 1 + C - 1) / C + 127) / 128, m + 1, m + 1);
-        return launch_pdl(k_prolong_correct3d<T>, g, dim3(128), 0, s, Lf, Lc, xi, xo, e, acc);
+        return launch_k(k_prolong_correct3d<T>, g, dim3(128), 0, s, Lf, Lc, xi, xo, e, acc);
     }
     return cudaGetLastError();
 }
@@ -502,8 +498,6 @@ __global__ void k_coarse_solve(Layout L, const T* __restrict__ b, T* __restrict_
     using O = Op<T>;
     extern __shared__ unsigned char smem_raw[];
     T* y = reinterpret_cast<T*>(smem_raw);
-    pdl_wait();
-    pdl_trigger();
     const int n = L.n;
     for (int q = threadIdx.x; q < nlu; q += blockDim.x) {
         const int i0 = L.dim == 2 ? q / n : q / (n * n);
@@ -551,7 +545,7 @@ cudaError_t launch_coarse_solve(const Layout& L, const T* b, T* x, const T* lu, 
         cudaError_t e = cudaFuncSetAttribute(k_coarse_solve<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    return launch_pdl(k_coarse_solve<T>, dim3(1), dim3(256), smem, s, L, b, x, lu, piv, nlu);
+    return launch_k(k_coarse_solve<T>, dim3(1), dim3(256), smem, s, L, b, x, lu, piv, nlu);
 }
 
 // ------------------------------------------------------------------------------------------

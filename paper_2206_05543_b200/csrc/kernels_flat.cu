@@ -22,8 +22,6 @@ __global__ void __launch_bounds__(256) k_rr2d_flat(Layout Lf, Layout Lc, const T
                                                    const T* __restrict__ b, T* __restrict__ bc, T sA) {
     constexpr int RH = 2 * F2_CH + 1, RW = 2 * F2_CW + 1, RP = RW + 1;
     __shared__ T rs[RH * RP];
-    pdl_wait();
-    pdl_trigger();
     const int n = Lf.n, m = Lc.n;
     const int I0 = blockIdx.y * F2_CH, J0 = blockIdx.x * F2_CW;
     const int f0 = 2 * I0, g0 = 2 * J0;  // fine interior index of local (0, 0)
@@ -55,8 +53,6 @@ __global__ void __launch_bounds__(256) k_rr3d_flat(Layout Lf, Layout Lc, const T
                                                    const T* __restrict__ b, T* __restrict__ bc, T sA) {
     constexpr int RZ = 2 * F3_CZ + 1, RY = 2 * F3_CY + 1, RX = 2 * F3_CX + 1, RP = RX + 1;
     __shared__ T rs[RZ * RY * RP];
-    pdl_wait();
-    pdl_trigger();
     const int n = Lf.n, m = Lc.n;
     const int I0 = blockIdx.z * F3_CZ, J0 = blockIdx.y * F3_CY, K0 = blockIdx.x * F3_CX;
     const int f0 = 2 * I0, f1 = 2 * J0, f2 = 2 * K0;
@@ -105,8 +101,6 @@ __global__ void __launch_bounds__(256) k_rr2d_flat_fz(Layout Lf, Layout Lc, cons
     constexpr int RH = 2 * BH + 1, RW = 2 * BW + 1, RP = RW + 1;  // fine r footprint
     __shared__ T rs[RH * RP];
     __shared__ T bs[BH * BW];
-    pdl_wait();
-    pdl_trigger();
     const int n = Lf.n, m = Lc.n;
     const int I0 = blockIdx.y * F2_CH - 1, J0 = blockIdx.x * F2_CW - 1;  // ring origin (coarse)
     const int f0 = 2 * I0, g0 = 2 * J0;
@@ -164,8 +158,6 @@ __global__ void __launch_bounds__(256) k_rr3d_flat_fz(Layout Lf, Layout Lc, cons
     constexpr int RZ = 2 * BZ + 1, RY = 2 * BY + 1, RX = 2 * BX + 1, RP = RX + 1;
     __shared__ T rs[RZ * RY * RP];
     __shared__ T bs[BZ * BY * BX];
-    pdl_wait();
-    pdl_trigger();
     const int n = Lf.n, m = Lc.n;
     const int I0 = blockIdx.z * CZ - 1, J0 = blockIdx.y * CY - 1, K0 = blockIdx.x * CX - 1;
     const int f0 = 2 * I0, f1 = 2 * J0, f2 = 2 * K0;
@@ -227,10 +219,10 @@ static cudaError_t rr_fz(const Layout& Lf, const Layout& Lc, const T* x, const T
     const int m = Lc.n;
     if (Lf.dim == 2) {
         dim3 g((m + F2_CW - 1) / F2_CW, (m + F2_CH - 1) / F2_CH);
-        return launch_pdl(k_rr2d_flat_fz<T, S>, g, dim3(256), 0, s, Lf, Lc, x, b, bc, xc, M, sA, sMc, omega);
+        return launch_k(k_rr2d_flat_fz<T, S>, g, dim3(256), 0, s, Lf, Lc, x, b, bc, xc, M, sA, sMc, omega);
     }
     dim3 g((m + 15) / 16, (m + 3) / 4, (m + 1) / 2);
-    return launch_pdl(k_rr3d_flat_fz<T, S>, g, dim3(128), 0, s, Lf, Lc, x, b, bc, xc, M, sA, sMc, omega);
+    return launch_k(k_rr3d_flat_fz<T, S>, g, dim3(128), 0, s, Lf, Lc, x, b, bc, xc, M, sA, sMc, omega);
 }
 
 template <class T>
@@ -259,192 +251,6 @@ template cudaError_t launch_residual_restrict_fz<float>(const Layout&, const Lay
                                                         float*, float*, const Terms<float>&, int, float, float, float,
                                                         cudaStream_t);
 
-// ------------------------------------------------------------------------------------------
-// K3 + K1 for the small levels: xo = sweep(x + P e) in one flat tile kernel.  The corrected
-// iterate xc = x + P e (multigrid.py:184; k_prolong_correct2d/3d trees) is formed on the tile
-// plus a 2-point halo in shared memory, r = b - A xc on the tile plus a 1-point halo, then
-// x' = xc + omega M r (multigrid.py:99-100).  Outside the interior P e and x are exactly 0 (zero
-// frames of both levels), as the reference's zero padding after the correction.
-// ------------------------------------------------------------------------------------------
-constexpr int P2_TW = 64, P2_TH = 16;
-constexpr int P3_TX = 32, P3_TY = 8, P3_TZ = 4;
-
-// (P e) at fine interior index (i0, i1[, i2]), separable, axis 0 first, reference end formulas
-template <class T>
-__device__ __forceinline__ T pe_point2(const Layout& Lc, const T* e, int i0, int i1) {
-    const int m = Lc.n;
-    auto at = [&](int j0, int j1) { return e[Lc.origin + (long long)j0 * Lc.px + j1]; };
-    auto t = [&](int j1) {
-        if (i0 & 1) return at((i0 - 1) >> 1, j1);
-        const int I = i0 >> 1;
-        return pl_even<T>(at(I - 1, j1), at(I, j1), I == 0, I == m);
-    };
-    if (i1 & 1) return t((i1 - 1) >> 1);
-    const int J = i1 >> 1;
-    return pl_even<T>(t(J - 1), t(J), J == 0, J == m);
-}
-
-template <class T>
-__device__ __forceinline__ T pe_point3(const Layout& Lc, const T* e, int i0, int i1, int i2) {
-    const int m = Lc.n;
-    auto at = [&](int j0, int j1, int j2) { return e[Lc.origin + (long long)j0 * Lc.pp + (long long)j1 * Lc.px + j2]; };
-    auto t0 = [&](int j1, int j2) {
-        if (i0 & 1) return at((i0 - 1) >> 1, j1, j2);
-        const int I = i0 >> 1;
-        return pl_even<T>(at(I - 1, j1, j2), at(I, j1, j2), I == 0, I == m);
-    };
-    auto t1 = [&](int j2) {
-        if (i1 & 1) return t0((i1 - 1) >> 1, j2);
-        const int J = i1 >> 1;
-        return pl_even<T>(t0(J - 1, j2), t0(J, j2), J == 0, J == m);
-    };
-    if (i2 & 1) return t1((i2 - 1) >> 1);
-    const int K = i2 >> 1;
-    return pl_even<T>(t1(K - 1), t1(K), K == 0, K == m);
-}
-
-template <class T, int S>
-__global__ void __launch_bounds__(256) k_sweep2d_tile_pc(Layout L, Layout Lc, const T* __restrict__ x,
-                                                         const T* __restrict__ e, const T* __restrict__ b,
-                                                         T* __restrict__ xo, Terms<T> M, T sA, T sM, T omega) {
-    using O = Op<T>;
-    constexpr int XW = P2_TW + 4, XH = P2_TH + 4, RW = P2_TW + 2, RH = P2_TH + 2;
-    __shared__ T xs[XH * XW];
-    __shared__ T rs[RH * RW];
-    pdl_wait();
-    pdl_trigger();
-    const int c0 = blockIdx.x * P2_TW, r0 = blockIdx.y * P2_TH;
-    const int n = L.n;
-    for (int q = threadIdx.x; q < XH * XW; q += blockDim.x) {
-        const int i0 = r0 - 2 + q / XW, i1 = c0 - 2 + q % XW;
-        const long long p = L.origin + (long long)i0 * L.px + i1;
-        // 0 + 0 on the frame; points past the frame are never read by an interior output
-        xs[q] = (i0 <= n + 1 && i1 <= n + 1) ? O::add(x[p], pe_point2<T>(Lc, e, i0, i1)) : T(0);
-    }
-    __syncthreads();
-    for (int q = threadIdx.x; q < RH * RW; q += blockDim.x) {
-        const int a0 = q / RW, a1 = q % RW;
-        const int i0 = r0 - 1 + a0, i1 = c0 - 1 + a1;
-        T rv = T(0);
-        if (i0 >= 0 && i0 < n && i1 >= 0 && i1 < n) {
-            const T* xc = xs + (a0 + 1) * XW + (a1 + 1);
-            rv = residual2d<T>(b[L.origin + (long long)i0 * L.px + i1], xc[0], xc[XW], xc[-XW], xc[1], xc[-1], sA);
-        }
-        rs[q] = rv;
-    }
-    __syncthreads();
-    for (int q = threadIdx.x; q < P2_TH * P2_TW; q += blockDim.x) {
-        const int a0 = q / P2_TW, a1 = q % P2_TW;
-        const int i0 = r0 + a0, i1 = c0 + a1;
-        if (i0 >= n || i1 >= n) continue;
-        T acc = T(0);
-        const int nt = tnt<T, S>(M);
-#pragma unroll
-        for (int k = 0; k < (S == SHAPE_GENERIC ? kMaxTerms : ShapeT<(S == SHAPE_GENERIC ? 1 : S)>::nt); ++k) {
-            if (S == SHAPE_GENERIC && k >= nt) break;
-            acc = O::add(acc, O::mul(M.c[k], rs[(a0 + 1 + toff<T, S>(M, k, 0)) * RW + (a1 + 1 + toff<T, S>(M, k, 1))]));
-        }
-        xo[L.origin + (long long)i0 * L.px + i1] = relax<T>(xs[(a0 + 2) * XW + (a1 + 2)], acc, sM, omega);
-    }
-}
-
-template <class T, int S>
-__global__ void __launch_bounds__(256) k_sweep3d_tile_pc(Layout L, Layout Lc, const T* __restrict__ x,
-                                                         const T* __restrict__ e, const T* __restrict__ b,
-                                                         T* __restrict__ xo, Terms<T> M, T sA, T sM, T omega) {
-    using O = Op<T>;
-    constexpr int XX = P3_TX + 4, XY = P3_TY + 4, XZ = P3_TZ + 4;
-    constexpr int RX = P3_TX + 2, RY = P3_TY + 2, RZ = P3_TZ + 2;
-    __shared__ T xs[XZ * XY * XX];
-    __shared__ T rs[RZ * RY * RX];
-    pdl_wait();
-    pdl_trigger();
-    const int x0 = blockIdx.x * P3_TX, y0 = blockIdx.y * P3_TY, z0 = blockIdx.z * P3_TZ;
-    const int n = L.n;
-    for (int q = threadIdx.x; q < XZ * XY * XX; q += blockDim.x) {
-        const int i0 = z0 - 2 + q / (XY * XX), i1 = y0 - 2 + (q / XX) % XY, i2 = x0 - 2 + q % XX;
-        const long long p = L.origin + (long long)i0 * L.pp + (long long)i1 * L.px + i2;
-        xs[q] = (i0 <= n + 1 && i1 <= n + 1 && i2 <= n + 1) ? O::add(x[p], pe_point3<T>(Lc, e, i0, i1, i2)) : T(0);
-    }
-    __syncthreads();
-    constexpr int SY = XX, SZ = XY * XX;
-    for (int q = threadIdx.x; q < RZ * RY * RX; q += blockDim.x) {
-        const int a0 = q / (RY * RX), a1 = (q / RX) % RY, a2 = q % RX;
-        const int i0 = z0 - 1 + a0, i1 = y0 - 1 + a1, i2 = x0 - 1 + a2;
-        T rv = T(0);
-        if (i0 >= 0 && i0 < n && i1 >= 0 && i1 < n && i2 >= 0 && i2 < n) {
-            const T* xc = xs + (a0 + 1) * SZ + (a1 + 1) * SY + (a2 + 1);
-            rv = residual3d<T>(b[L.origin + (long long)i0 * L.pp + (long long)i1 * L.px + i2], xc[0], xc[SZ], xc[-SZ],
-                               xc[SY], xc[-SY], xc[1], xc[-1], sA);
-        }
-        rs[q] = rv;
-    }
-    __syncthreads();
-    for (int q = threadIdx.x; q < P3_TZ * P3_TY * P3_TX; q += blockDim.x) {
-        const int a0 = q / (P3_TY * P3_TX), a1 = (q / P3_TX) % P3_TY, a2 = q % P3_TX;
-        const int i0 = z0 + a0, i1 = y0 + a1, i2 = x0 + a2;
-        if (i0 >= n || i1 >= n || i2 >= n) continue;
-        T acc = T(0);
-        const int nt = tnt<T, S>(M);
-#pragma unroll
-        for (int k = 0; k < (S == SHAPE_GENERIC ? kMaxTerms : ShapeT<(S == SHAPE_GENERIC ? 1 : S)>::nt); ++k) {
-            if (S == SHAPE_GENERIC && k >= nt) break;
-            const int o0 = toff<T, S>(M, k, 0), o1 = toff<T, S>(M, k, 1), o2 = toff<T, S>(M, k, 2);
-            acc = O::add(acc, O::mul(M.c[k], rs[((a0 + 1 + o0) * RY + (a1 + 1 + o1)) * RX + (a2 + 1 + o2)]));
-        }
-        xo[L.origin + (long long)i0 * L.pp + (long long)i1 * L.px + i2] =
-            relax<T>(xs[(a0 + 2) * SZ + (a1 + 2) * SY + (a2 + 2)], acc, sM, omega);
-    }
-}
-
-template <class T, int S>
-static cudaError_t pc_tile(const Layout& L, const Layout& Lc, const T* x, const T* e, const T* b, T* xo,
-                           const Terms<T>& M, T sA, T sM, T omega, cudaStream_t s) {
-    const int n = L.n;
-    if (L.dim == 2) {
-        dim3 g((n + P2_TW - 1) / P2_TW, (n + P2_TH - 1) / P2_TH);
-        return launch_pdl(k_sweep2d_tile_pc<T, S>, g, dim3(256), 0, s, L, Lc, x, e, b, xo, M, sA, sM, omega);
-    }
-    dim3 g((n + P3_TX - 1) / P3_TX, (n + P3_TY - 1) / P3_TY, (n + P3_TZ - 1) / P3_TZ);
-    return launch_pdl(k_sweep3d_tile_pc<T, S>, g, dim3(256), 0, s, L, Lc, x, e, b, xo, M, sA, sM, omega);
-}
-
-template <class T>
-cudaError_t launch_sweep_pc_flat(const Layout& L, const Layout& Lc, const T* x, const T* e, const T* b, T* xo,
-                                 const Terms<T>& M, int shape, T sA, T sM, T omega, cudaStream_t s) {
-    switch (shape) {
-        case SHAPE_C1: return pc_tile<T, SHAPE_C1>(L, Lc, x, e, b, xo, M, sA, sM, omega, s);
-        case SHAPE_STAR5:
-            if (L.dim == 2) return pc_tile<T, SHAPE_STAR5>(L, Lc, x, e, b, xo, M, sA, sM, omega, s);
-            break;
-        case SHAPE_BOX9:
-            if (L.dim == 2) return pc_tile<T, SHAPE_BOX9>(L, Lc, x, e, b, xo, M, sA, sM, omega, s);
-            break;
-        case SHAPE_STAR7:
-            if (L.dim == 3) return pc_tile<T, SHAPE_STAR7>(L, Lc, x, e, b, xo, M, sA, sM, omega, s);
-            break;
-        default: break;
-    }
-    return pc_tile<T, SHAPE_GENERIC>(L, Lc, x, e, b, xo, M, sA, sM, omega, s);
-}
-
-template cudaError_t launch_sweep_pc_flat<double>(const Layout&, const Layout&, const double*, const double*,
-                                                  const double*, double*, const Terms<double>&, int, double, double,
-                                                  double, cudaStream_t);
-template cudaError_t launch_sweep_pc_flat<float>(const Layout&, const Layout&, const float*, const float*, const float*,
-                                                 float*, const Terms<float>&, int, float, float, float, cudaStream_t);
-
-bool pdl_enabled() {
-    static int on = -1;
-    if (on < 0) {
-        // measured neutral-to-slightly-negative on the c1-c4 cycles (launch latency is not the
-        // bottleneck of the small levels; their memory latency is), so opt-in
-        const char* e = getenv("SPAIMG_PDL");
-        on = (e && e[0] == '1') ? 1 : 0;
-    }
-    return on == 1;
-}
-
 int flat_threshold(int dim) {
     const char* e = getenv(dim == 2 ? "SPAIMG_FLAT_N2" : "SPAIMG_FLAT_N3");
     if (e) return atoi(e);
@@ -457,10 +263,10 @@ cudaError_t launch_residual_restrict_flat(const Layout& Lf, const Layout& Lc, co
     const int m = Lc.n;
     if (Lf.dim == 2) {
         dim3 g((m + F2_CW - 1) / F2_CW, (m + F2_CH - 1) / F2_CH);
-        return launch_pdl(k_rr2d_flat<T>, g, dim3(256), 0, s, Lf, Lc, x, b, bc, sA);
+        return launch_k(k_rr2d_flat<T>, g, dim3(256), 0, s, Lf, Lc, x, b, bc, sA);
     } else {
         dim3 g((m + F3_CX - 1) / F3_CX, (m + F3_CY - 1) / F3_CY, (m + F3_CZ - 1) / F3_CZ);
-        return launch_pdl(k_rr3d_flat<T>, g, dim3(256), 0, s, Lf, Lc, x, b, bc, sA);
+        return launch_k(k_rr3d_flat<T>, g, dim3(256), 0, s, Lf, Lc, x, b, bc, sA);
     }
     return cudaGetLastError();
 }

@@ -103,8 +103,6 @@ __global__ void __launch_bounds__((R2_NW + 1) * 32) k_residual_restrict2d(Layout
     constexpr int V = R2<T>::V;
     constexpr int CW = R2<T>::CW;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    pdl_wait();
-    pdl_trigger();
     R2Ctx<T> c;
     c.xs = reinterpret_cast<T*>(smem_raw);
     c.bs = c.xs + R2_ST * RW;
@@ -176,7 +174,7 @@ cudaError_t launch_residual_restrict2d_march(const Layout& Lf, const Layout& Lc,
     const int rows = (m + chunks - 1) / chunks;
     chunks = (m + rows - 1) / rows;
     dim3 g(strips, chunks);
-    return launch_pdl(k_residual_restrict2d<T>, g, dim3(threads), smem, s, Lf, Lc, x, b, bc, sA, rows);
+    return launch_k(k_residual_restrict2d<T>, g, dim3(threads), smem, s, Lf, Lc, x, b, bc, sA, rows);
 }
 
 template cudaError_t launch_residual_restrict2d_march<double>(const Layout&, const Layout&, const double*,

@@ -28,8 +28,6 @@ __global__ void __launch_bounds__(256) k_sweep2d_tile(Layout L, const T* __restr
     using O = Op<T>;
     constexpr int RW = S2_TW + 2, RH = S2_TH + 2;
     __shared__ T rs[RH * RW];
-    pdl_wait();
-    pdl_trigger();
     const int c0 = blockIdx.x * S2_TW, r0 = blockIdx.y * S2_TH;
     const int n = L.n;
     for (int q = threadIdx.x; q < RH * RW; q += blockDim.x) {
@@ -69,8 +67,6 @@ __global__ void __launch_bounds__(256) k_sweep3d_tile(Layout L, const T* __restr
     using O = Op<T>;
     constexpr int RX = S3_TX + 2, RY = S3_TY + 2, RZ = S3_TZ + 2;
     __shared__ T rs[RZ * RY * RX];
-    pdl_wait();
-    pdl_trigger();
     const int x0 = blockIdx.x * S3_TX, y0 = blockIdx.y * S3_TY, z0 = blockIdx.z * S3_TZ;
     const int n = L.n;
     for (int q = threadIdx.x; q < RZ * RY * RX; q += blockDim.x) {
@@ -344,8 +340,6 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, co
     constexpr int RW = m2_rowlen<T>();
     constexpr int ST = M2_ST;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    pdl_wait();
-    pdl_trigger();
     M2Ctx<T> c;
     c.xs = reinterpret_cast<T*>(smem_raw);
     c.bs = c.xs + ST * RW;
@@ -441,7 +435,7 @@ static cudaError_t launch_sweep2d_march(const Layout& L, const T* x, const T* b,
     const int rows = (L.n + chunks - 1) / chunks;
     chunks = (L.n + rows - 1) / rows;
     dim3 g(strips, chunks);
-    return launch_pdl(k_sweep2d_march<T, S, FZ, NM>, g, dim3(threads), smem, s, L, x, b, xo, M, sA, sM, omega, rows,
+    return launch_k(k_sweep2d_march<T, S, FZ, NM>, g, dim3(threads), smem, s, L, x, b, xo, M, sA, sM, omega, rows,
                       no, e, Lc ? *Lc : L);
 }
 
@@ -454,24 +448,21 @@ template <class T, int S, bool FZ, int NM>
 cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
                                  T omega, const NormOut& no, cudaStream_t s, const Layout* Lc = nullptr);
 
-static bool sweep_v1() { return getenv("SPAIMG_SWEEP_V1") != nullptr; }
-bool sweep_norm_supported() { return !sweep_v1(); }
-
 template <class T, int S, bool FZ, int NM>
 static cudaError_t sweep_dispatch(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
                                   T omega, const NormOut& no, cudaStream_t s) {
     constexpr int S3 = (S == SHAPE_GENERIC || S == SHAPE_C1 || S == SHAPE_STAR7) ? S : SHAPE_GENERIC;
     const bool flat = NM == 0 && L.N <= flat_threshold(L.dim);
     if (L.dim == 2) {
-        if ((sweep_v1() || flat) && NM == 0) {
+        if (flat && NM == 0) {
             dim3 g((L.n + S2_TW - 1) / S2_TW, (L.n + S2_TH - 1) / S2_TH);
-            return launch_pdl(k_sweep2d_tile<T, S, FZ>, g, dim3(256), 0, s, L, x, b, xo, M, sA, sM, omega);
+            return launch_k(k_sweep2d_tile<T, S, FZ>, g, dim3(256), 0, s, L, x, b, xo, M, sA, sM, omega);
         }
         return launch_sweep2d_march<T, S, FZ, NM>(L, x, b, xo, M, sA, sM, omega, no, s);
     }
-    if ((sweep_v1() || flat) && NM == 0) {
+    if (flat && NM == 0) {
         dim3 g((L.n + S3_TX - 1) / S3_TX, (L.n + S3_TY - 1) / S3_TY, (L.n + S3_TZ - 1) / S3_TZ);
-        return launch_pdl(k_sweep3d_tile<T, S, FZ>, g, dim3(256), 0, s, L, x, b, xo, M, sA, sM, omega);
+        return launch_k(k_sweep3d_tile<T, S, FZ>, g, dim3(256), 0, s, L, x, b, xo, M, sA, sM, omega);
     }
     return launch_sweep3d_march<T, S3, FZ, NM>(L, x, b, xo, M, sA, sM, omega, no, s);
 }
@@ -506,28 +497,17 @@ cudaError_t launch_sweep(const Layout& L, const T* x, const T* b, T* xo, const T
     return sweep_fz<T, SHAPE_GENERIC>(L, x, b, xo, M, sA, sM, omega, from_zero, no, s);
 }
 
-// K3 + K1 fused: xo = sweep(x + P e) for the first post-smoothing step (multigrid.py:184-185);
-// 2D marching levels only (the prolongation is applied to every staged x value on the fly)
-// 2D marching levels: the marching kernel with the correction applied to every staged x row
-// (NM == 3); flat levels (opt-in, SPAIMG_PC_FLAT=1): k_sweep{2,3}d_tile_pc (kernels_flat.cu).
-// Measured (tools/tune.py): the marching fusion is a net win on the 4096^2 level (-16 B/unknown
-// of HBM traffic) and a loss on 2048^2 (its extra per-step work is not hidden once the level's
-// HBM time is short); the flat fusion is neutral in 2D and a loss in 3D (small levels are bound
-// by the latency of their dependent loads, which the fusion lengthens).
-bool sweep_pc_supported(const Layout& L) {
-    const char* e = getenv("SPAIMG_PC");
-    if (sweep_v1() || (e && e[0] == '0')) return false;
-    if (L.N <= flat_threshold(L.dim)) {
-        const char* f = getenv("SPAIMG_PC_FLAT");
-        return f && f[0] == '1';
-    }
-    return L.dim == 2 && L.N > 2048;
-}
+// K3 + K1 fused: xo = sweep(x + P e) for the first post-smoothing step (multigrid.py:184-185),
+// on 2D marching levels: the marching kernel with the correction applied to every staged x row
+// (NM == 3).  Measured (tools/tune.py): a net win on the 4096^2 level (-16 B/unknown of HBM
+// traffic) and a loss on 2048^2, where its extra per-step work is not hidden once the level's
+// HBM time is short.  (A flat-tile fusion for the small levels was measured neutral in 2D and a
+// loss in 3D, and removed.)
+bool sweep_pc_supported(const Layout& L) { return L.dim == 2 && L.N > 2048; }
 
 template <class T>
 cudaError_t launch_sweep_pc(const Layout& L, const Layout& Lc, const T* x, const T* e, const T* b, T* xo,
                             const Terms<T>& M, int shape, T sA, T sM, T omega, cudaStream_t s) {
-    if (L.N <= flat_threshold(L.dim)) return launch_sweep_pc_flat<T>(L, Lc, x, e, b, xo, M, shape, sA, sM, omega, s);
     const NormOut none{};
     switch (shape) {
         case SHAPE_C1: return launch_sweep2d_march<T, SHAPE_C1, false, 3>(L, x, b, xo, M, sA, sM, omega, none, s, e, &Lc);
@@ -549,7 +529,7 @@ cudaError_t launch_norm_march(const Layout& L, const T* x, const T* b, T sA, con
 }
 
 // ------------------------------------------------------------------------------------------
-// K2 v1: residual into scratch, then restriction
+// K2 dispatch: flat tile kernels on small levels, the row march in 2D, the plane march in 3D
 // ------------------------------------------------------------------------------------------
 template <class T>
 cudaError_t launch_residual_restrict2d_march(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T sA,
@@ -557,18 +537,11 @@ cudaError_t launch_residual_restrict2d_march(const Layout& Lf, const Layout& Lc,
 
 template <class T>
 cudaError_t launch_residual_restrict(const Layout& Lf, const Layout& Lc, const T* x, const T* b, T* bc, T sA,
-                                     T* scratch_r, cudaStream_t s) {
-    if (Lf.N <= flat_threshold(Lf.dim) && !getenv("SPAIMG_RESTRICT_V1"))
-        return launch_residual_restrict_flat<T>(Lf, Lc, x, b, bc, sA, s);
-    if (Lf.dim == 2 && !getenv("SPAIMG_RESTRICT_V1"))
-        return launch_residual_restrict2d_march<T>(Lf, Lc, x, b, bc, sA, s);
-    if (Lf.dim == 3 && !getenv("SPAIMG_RESTRICT_V1")) {
-        const Terms<T> none{};
-        return launch_sweep3d_march<T, SHAPE_C1, false, 3>(Lf, x, b, bc, none, sA, T(0), T(0), NormOut{}, s, &Lc);
-    }
-    cudaError_t e = launch_residual<T>(Lf, x, b, scratch_r, sA, s);
-    if (e != cudaSuccess) return e;
-    return launch_restrict<T>(Lf, Lc, scratch_r, bc, s);
+                                     cudaStream_t s) {
+    if (Lf.N <= flat_threshold(Lf.dim)) return launch_residual_restrict_flat<T>(Lf, Lc, x, b, bc, sA, s);
+    if (Lf.dim == 2) return launch_residual_restrict2d_march<T>(Lf, Lc, x, b, bc, sA, s);
+    const Terms<T> none{};
+    return launch_sweep3d_march<T, SHAPE_C1, false, 3>(Lf, x, b, bc, none, sA, T(0), T(0), NormOut{}, s, &Lc);
 }
 
 template cudaError_t launch_sweep<double>(const Layout&, const double*, const double*, double*, const Terms<double>&,
@@ -585,8 +558,8 @@ template cudaError_t launch_norm_march<double>(const Layout&, const double*, con
 template cudaError_t launch_norm_march<float>(const Layout&, const float*, const float*, float, const NormOut&,
                                               cudaStream_t);
 template cudaError_t launch_residual_restrict<double>(const Layout&, const Layout&, const double*, const double*,
-                                                      double*, double, double*, cudaStream_t);
+                                                      double*, double, cudaStream_t);
 template cudaError_t launch_residual_restrict<float>(const Layout&, const Layout&, const float*, const float*, float*,
-                                                     float, float*, cudaStream_t);
+                                                     float, cudaStream_t);
 
 }  // namespace spaimg

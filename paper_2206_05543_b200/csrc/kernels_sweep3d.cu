@@ -302,8 +302,6 @@ __global__ void __launch_bounds__(M3_THREADS, 2)
     using G = M3<T>;
     constexpr int VEC = G::VEC;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    pdl_wait();
-    pdl_trigger();
     M3Ctx<T> c;
     c.xs = reinterpret_cast<T*>(smem_raw);
     c.bs = c.xs + M3_ST * G::XS;
@@ -435,7 +433,7 @@ cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo,
     const int planes = (span + chunks - 1) / chunks;
     chunks = (span + planes - 1) / planes;
     dim3 g(tx, ty, chunks);
-    return launch_pdl(k_sweep3d_march<T, S, FZ, NM>, g, dim3(M3_THREADS), G::smem, s, L, xm, bm, x, xo, M, sA, sM,
+    return launch_k(k_sweep3d_march<T, S, FZ, NM>, g, dim3(M3_THREADS), G::smem, s, L, xm, bm, x, xo, M, sA, sM,
                       omega, planes, no, Lc ? *Lc : L);
 }
 

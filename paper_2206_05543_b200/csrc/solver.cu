@@ -187,9 +187,6 @@ static int alloc_level(Scratch& sc, Level<T>& lv, int dim, int N, bool two_x, bo
     return 0;
 }
 
-// kernel launches of one residual+restriction (2D: one fused marching kernel)
-static int residual_restrict_launches(int) { return !getenv("SPAIMG_RESTRICT_V1") ? 1 : 2; }
-
 // one smoothing step on a level: x[a] -> x[1-a]
 template <class T>
 static int do_sweep(Level<T>& lv, int a, bool fz, const Terms<T>& M, int shape, bool fused, T omega, cudaStream_t s,
@@ -334,11 +331,11 @@ template <class T>
 static int residual_restrict_t(int dim, int N, const void* u, const void* b, void* coarse, cudaStream_t s) {
     Scratch sc(s);
     Level<T> f, c;
-    if (int rc = alloc_level<T>(sc, f, dim, N, false, true, true)) return rc;
+    if (int rc = alloc_level<T>(sc, f, dim, N, false, true, false)) return rc;
     if (int rc = alloc_level<T>(sc, c, dim, N / 2, false, false, false)) return rc;
     if (int rc = load_dense<T>(sc, f.L, u, f.x[0], s)) return rc;
     if (int rc = load_dense<T>(sc, f.L, b, f.b, s)) return rc;
-    CK(launch_residual_restrict<T>(f.L, c.L, f.x[0], f.b, c.x[0], f.sA, f.r, s));
+    CK(launch_residual_restrict<T>(f.L, c.L, f.x[0], f.b, c.x[0], f.sA, s));
     return store_dense<T>(sc, c.L, c.x[0], coarse, s);
 }
 
@@ -393,32 +390,18 @@ struct spaimg_solver {
 };
 
 // ------------------------------------------------------------------------------------------
-// device-side solve loop (reference multigrid.py:206-217) as a CUDA graph with conditional
-// nodes:   reset -> WHILE(cont) { A: norm of u_k (fused into cycle k+1's first pre-sweep);
-//                                 check: cont = !(k>=1 && ||r_k|| <= tol ||r_0||) && k < max;
-//                                 IF(cont) { B: rest of cycle k+1 } }
-// No host round trip per cycle; the history stays on the device until the loop ends.
+// device-side solve loop (reference multigrid.py:206-217) as a CUDA graph with a conditional
+// WHILE node:   reset -> A -> WHILE(cont) { B -> A }
+// A = the norm of u_k fused into cycle k+1's first pre-sweep (which only writes the other
+// buffer, so it is harmlessly speculative after the last cycle); the norm kernel's last CTA
+// runs the stop test (‖r_k‖ <= tol ‖r_0‖ or k == max_iters) and sets the WHILE condition.
+// B = the rest of cycle k+1.  No host round trip per cycle; the history stays on the device.
 // ------------------------------------------------------------------------------------------
 
 __global__ void k_solve_reset(int* slot, int* state) {
-    pdl_wait();
-    pdl_trigger();
     *slot = 0;
     state[0] = 0;
     state[1] = 0;
-}
-
-__global__ void k_solve_check(const double* norms, const int* slot, const SolveCtl* ctl, int* state,
-                              cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hi) {
-    pdl_wait();
-    pdl_trigger();
-    const int k = *slot - 1;  // norms[0..k] are known: k cycles done
-    const bool conv = k >= 1 && norms[k] <= ctl->tol * norms[0];
-    const bool cont = !conv && k < ctl->max_iters;
-    state[0] = k;
-    state[1] = conv ? 1 : 0;
-    cudaGraphSetConditional(hw, cont ? 1u : 0u);
-    cudaGraphSetConditional(hi, cont ? 1u : 0u);
 }
 
 template <class T> struct Solver final : spaimg_solver {
@@ -430,7 +413,6 @@ template <class T> struct Solver final : spaimg_solver {
     int shape = SHAPE_GENERIC;
     bool fused = false;      // fused K1 sweep available for this smoother
     bool fused_norm = false; // norm folded into the first pre-sweep (A) of the next cycle
-    bool a_rr = false;       // A also carries level 0's residual + restriction (K1+K2 march)
     bool k3_flip = false;    // (nu1+nu2) odd: the finest K3 writes the other buffer so a cycle ends in x[0]
     T omega{};
     T* lu = nullptr;
@@ -453,14 +435,13 @@ template <class T> struct Solver final : spaimg_solver {
     bool use_graph = true;
     std::vector<void*> owned;
     std::vector<std::pair<long long, cudaGraphExec_t>> op_graphs;
-    // single-block shared-memory tail: levels >= tail_l (if < nsmooth()) run in one CTA per visit
+    // shared-memory coarse engine (K5+): levels >= tail_l (if < nsmooth()) run in one CTA per visit
     int tail_l = 1 << 30;
-    TailLevel<T>* tail_lv = nullptr;  // device copy of the tail levels' shared-memory descriptors
-    TailOp* tail_ops[2][2] = {};      // uploaded op lists keyed by (entry buffer a, zero start)
-    int tail_nops[2][2] = {};
-    int tail_out[2][2] = {};
-    int tail_nlv = 0, tail_elems = 0;
-    size_t tail_arr_off = 0, tail_smem = 0;
+    TailOp<T>* tail_ops[2] = {};  // uploaded op lists for an entry from a given iterate / from zero
+    int tail_nops[2] = {};
+    T* tail_coarse = nullptr;     // coarse LU data in the engine's format
+    int* tail_coarse_idx = nullptr;
+    TailArgs<T> tail_args{};      // everything but the op list and the entry buffers
 
     ~Solver() override {
         if (bs_h2d) {
@@ -482,6 +463,7 @@ template <class T> struct Solver final : spaimg_solver {
         for (auto& kv : op_graphs) cudaGraphExecDestroy(kv.second);
         for (void* p : owned) cudaFree(p);
         if (norms_h) cudaFreeHost(norms_h);
+        if (state_h) cudaFreeHost(state_h);
     }
 
     template <class U> int dalloc(U** p, size_t count) {
@@ -499,8 +481,8 @@ template <class T> struct Solver final : spaimg_solver {
     NormOut norm_sink_cond(cudaGraphConditionalHandle h) const {
         return NormOut{partials, counter, norms_d, slot_d, ctl_d, state_d, h};
     }
-    cudaGraphConditionalHandle cur_cond = 0;  // set while capturing the solve graph (fold mode)
-    bool fold_check = false;
+    cudaGraphConditionalHandle cur_cond = 0;  // set while capturing the solve graph
+    bool in_solve_graph = false;
 
     int init(const spaimg_mg_config& c) {
         cfg = c;
@@ -527,7 +509,7 @@ template <class T> struct Solver final : spaimg_solver {
             if (int rc = dalloc(&l.b, (size_t)l.L.alloc)) return rc;
             if (!coarse) {
                 if (int rc = dalloc(&l.x[1], (size_t)l.L.alloc)) return rc;
-                if (!fused || getenv("SPAIMG_RESTRICT_V1") || N <= std::max(tail_threshold(c), cluster_threshold(c)))
+                if (!fused)  // the unfused residual + relax sweep (stencil radius 2)
                     if (int rc = dalloc(&l.r, (size_t)l.L.alloc)) return rc;
             }
             lv.push_back(l);
@@ -538,8 +520,7 @@ template <class T> struct Solver final : spaimg_solver {
         }
         if (N != c.coarse_N || count_of(c.dim, N) != c.coarse_n)
             return fail(SPAIMG_EINVAL, "coarse factorisation does not match the coarsest level");
-        fused_norm = nsmooth() >= 1 && c.nu1 >= 1 && fused && sweep_norm_supported();
-        a_rr = fused_norm && c.nu1 == 1 && sweep_rr_supported(lv[0].L);
+        fused_norm = nsmooth() >= 1 && c.nu1 >= 1 && fused;
         nlu = c.coarse_n;
         std::vector<T> luT(lu_h.begin(), lu_h.end());
         if (int rc = dalloc(&lu, luT.size())) return rc;
@@ -547,328 +528,306 @@ template <class T> struct Solver final : spaimg_solver {
         if (int rc = dalloc(&piv, piv_h.size())) return rc;
         CK(cudaMemcpy(piv, piv_h.data(), piv_h.size() * sizeof(int), cudaMemcpyHostToDevice));
         if (int rc = init_tail()) return rc;
-        if (int rc = init_cluster()) return rc;
-        norms_cap = 4097;
-        if (int rc = dalloc(&norms_d, norms_cap)) return rc;
+        norms_cap = 0;
+        if (int rc = grow_norms(101)) return rc;  // the reference default max_iters = 100; grown on demand
         if (int rc = dalloc(&slot_d, 1)) return rc;
         if (int rc = dalloc(&state_d, 2)) return rc;
         if (int rc = dalloc(&ctl_d, 1)) return rc;
         if (int rc = dalloc(&partials, 1 << 16)) return rc;
         if (int rc = dalloc(&counter, 1)) return rc;
         if (int rc = dalloc(&stage, (size_t)count_of(c.dim, c.N))) return rc;
-        // one pinned block: norms | state | ctl
         void* ph = nullptr;
-        CK(cudaMallocHost(&ph, sizeof(double) * norms_cap + 64 + sizeof(SolveCtl)));
-        norms_h = static_cast<double*>(ph);
-        state_h = reinterpret_cast<int*>(norms_h + norms_cap);
-        ctl_h = reinterpret_cast<SolveCtl*>(reinterpret_cast<char*>(state_h) + 64);
+        CK(cudaMallocHost(&ph, 64 + sizeof(SolveCtl)));
+        state_h = static_cast<int*>(ph);
+        ctl_h = reinterpret_cast<SolveCtl*>(static_cast<char*>(ph) + 64);
+        // every buffer above was zeroed on the legacy stream; the solver runs on the caller's
+        // (possibly non-blocking) stream, so finish that work before returning
+        CK(cudaDeviceSynchronize());
+        return 0;
+    }
+
+    // residual-history buffers for at least `cap` norms (device + pinned host).  The graphs read
+    // norms_d through NormOut by value, so growing re-captures them.
+    int grow_norms(int cap) {
+        if (cap <= norms_cap) return 0;
+        double* d = nullptr;
+        CK(cudaMalloc(&d, sizeof(double) * cap));
+        CK(cudaMemset(d, 0, sizeof(double) * cap));
+        double* h = nullptr;
+        CK(cudaMallocHost(&h, sizeof(double) * cap));
+        if (norms_d) {
+            CK(cudaMemcpy(d, norms_d, sizeof(double) * norms_cap, cudaMemcpyDeviceToDevice));
+            cudaFree(norms_d);
+            owned.erase(std::remove(owned.begin(), owned.end(), (void*)norms_d), owned.end());
+        }
+        if (norms_h) cudaFreeHost(norms_h);
+        norms_d = d;
+        norms_h = h;
+        owned.push_back(d);
+        norms_cap = cap;
+        if (exec_cycle) cudaGraphExecDestroy(exec_cycle);
+        if (exec_solve) cudaGraphExecDestroy(exec_solve);
+        exec_cycle = exec_solve = nullptr;
+        for (auto& kv : op_graphs) cudaGraphExecDestroy(kv.second);
+        op_graphs.clear();
         return 0;
     }
 
     int nsmooth() const { return (int)lv.size() - 1; }
 
-    // largest mesh count run by the shared-memory tail kernel (SPAIMG_TAIL_N overrides; 0 disables)
+    // largest mesh count run by the shared-memory engine (SPAIMG_TAIL_N overrides; 0 disables).
+    // The engine maps a level onto a box of at most 64^2 / 16^3 points.
     static int tail_threshold(const spaimg_mg_config& c) {
         const char* e = getenv("SPAIMG_TAIL_N");
         if (e) return atoi(e);
-        return c.dim == 2 ? 32 : 8;  // measured optimum (tools/tune.py c1-c4)
+        return c.dim == 2 ? 64 : 16;
     }
 
-    // compact shared-memory layout of an n^dim level with a zero frame of F cells
-    static Layout smem_layout(int dim, int N, int F) {
-        Layout L{};
-        L.dim = dim;
-        L.N = N;
-        L.n = N - 1;
-        L.esize = sizeof(T);
-        const long long w = L.n + 2 * F;
-        L.px = w;
-        L.pp = dim == 3 ? w * w : 0;
-        L.origin = dim == 3 ? F * L.pp + F * w + F : F * w + F;
-        L.alloc = dim == 3 ? w * w * w : w * w;
-        return L;
+    // ---- shared-memory engine plan ------------------------------------------------------
+    struct TGeo {
+        int n, logw, w, s0, s1, x, b, r;
+        T sA, sM;
+    };
+    std::vector<TGeo> tg;  // tail levels: tg[0] = entry level ... tg.back() = coarse level
+
+    static int ceil_log2(int n) {
+        int k = 0;
+        while ((1 << k) < n) ++k;
+        return k;
+    }
+    static int warps_for(int dim, int logw) {
+        const long long pts = 1LL << (dim * logw);
+        const long long act = pts > kTailThreads ? kTailThreads : pts;
+        return (int)((act + 31) / 32);
+    }
+
+    // levels l0 .. nsmooth() in shared memory: geometry; returns the array block size (elements)
+    int plan_geometry(int l0, int F, int* zero_from) {
+        tg.clear();
+        int cur = 0;
+        for (int l = l0; l <= nsmooth(); ++l) {
+            TGeo g{};
+            g.n = lv[l].L.n;
+            g.logw = ceil_log2(g.n);
+            g.w = g.n + 2 * F;
+            g.s0 = cfg.dim == 2 ? g.w : g.w * g.w;
+            g.s1 = cfg.dim == 3 ? g.w : 0;
+            const int size = (cfg.dim == 2 ? g.w * g.w : g.w * g.w * g.w + 1) / 2 * 2;  // 16-byte multiples
+            const int origin = F * g.s0 + F * g.s1 + F;
+            g.x = cur + origin;
+            cur += size;
+            g.b = cur + origin;
+            cur += size;
+            if (l == l0) *zero_from = cur;
+            if (l < nsmooth()) {
+                g.r = cur + origin;
+                cur += size;
+            } else {
+                g.r = -1;
+            }
+            g.sA = lv[l].sA;
+            g.sM = lv[l].sM;
+            tg.push_back(g);
+        }
+        // strips may read up to two axis-0 rows past an array (values unused): keep them in bounds
+        return cur + 2 * tg[0].s0 + 2 * tg[0].s1 + 2;
+    }
+
+    TailOp<T> point_op(int type, int i) const {
+        const TGeo& g = tg[i];
+        TailOp<T> o{};
+        o.type = type;
+        o.logw = g.logw;
+        o.nw = warps_for(cfg.dim, g.logw);
+        o.n = g.n;
+        o.s0 = g.s0;
+        o.s1 = g.s1;
+        o.a0 = g.x;
+        o.a1 = g.b;
+        o.a2 = g.r;
+        o.s = type == TAIL_RES ? g.sA : g.sM;
+        if (type == TAIL_FW || type == TAIL_PROLONG) {
+            const TGeo& c = tg[i + 1];
+            o.nw = type == TAIL_FW ? warps_for(cfg.dim, g.logw - 1) : o.nw;
+            o.a1 = type == TAIL_FW ? c.b : c.x;
+            o.m = c.n;
+            o.cs0 = c.s0;
+            o.cs1 = c.s1;
+        }
+        return o;
+    }
+
+    // the recursion of visit() (multigrid.py:157-185) below the entry level, as engine ops
+    void record(int i, bool fz, std::vector<TailOp<T>>& ops) const {
+        const int last = (int)tg.size() - 1;
+        if (i == last) {  // u.N <= coarsest_N: direct solve (multigrid.py:166-167)
+            TailOp<T> o{};
+            o.type = TAIL_COARSE;
+            o.nw = (nlu == 1 || nlu == 9 || nlu == 27 || nlu <= 32) ? 1 : kTailThreads / 32;
+            o.n = tg[i].n;
+            o.a0 = tg[i].x;
+            o.a1 = tg[i].b;
+            ops.push_back(o);
+            return;
+        }
+        for (int k = 0; k < cfg.nu1; ++k) {
+            if (fz && k == 0) {
+                ops.push_back(point_op(TAIL_RELAX0, i));
+            } else {
+                ops.push_back(point_op(TAIL_RES, i));
+                ops.push_back(point_op(TAIL_RELAX, i));
+            }
+        }
+        if (fz && cfg.nu1 == 0) ops.push_back(point_op(TAIL_ZERO, i));
+        ops.push_back(point_op(TAIL_RES, i));
+        ops.push_back(point_op(TAIL_FW, i));
+        record(i + 1, true, ops);
+        for (int g = 1; g < cfg.gamma; ++g) record(i + 1, false, ops);
+        ops.push_back(point_op(TAIL_PROLONG, i));
+        for (int k = 0; k < cfg.nu2; ++k) {
+            ops.push_back(point_op(TAIL_RES, i));
+            ops.push_back(point_op(TAIL_RELAX, i));
+        }
+    }
+
+    // barrier plan: op i waits with the warps of ops i-1 and i (always a prefix of the CTA); one
+    // named barrier id per distinct warp count -- warps that skip small ops run ahead and must
+    // not share a barrier with a different count
+    int tail_barriers(std::vector<TailOp<T>>& ops) const {
+        std::vector<int> counts;
+        const int all = kTailThreads / 32;
+        int prev = all;
+        for (TailOp<T>& o : ops) {
+            o.bw = std::max(o.nw, prev);
+            prev = o.nw;
+            if (o.bw == all) {
+                o.bid = 0;
+            } else if (o.bw == 1) {
+                o.bid = -1;
+            } else {
+                auto it = std::find(counts.begin(), counts.end(), o.bw);
+                if (it == counts.end()) {
+                    counts.push_back(o.bw);
+                    it = counts.end() - 1;
+                }
+                o.bid = (int)(it - counts.begin()) + 1;
+            }
+        }
+        if (counts.size() > 15) return fail(SPAIMG_ENOTSUP, "tail: too many distinct warp counts for named barriers");
+        return 0;
     }
 
     int init_tail() {
         const int thr = tail_threshold(cfg);
         if (thr <= 0) return 0;
         const int F = std::max(1, stencil_radius(cfg.M));
+        if (F > kGhost) return 0;
+        const int nmax = cfg.dim == 2 ? 63 : 15;  // the engine's largest W^dim box
         int dev = 0, optin = 0;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         int l0 = nsmooth();
-        while (l0 > 1 && lv[l0 - 1].L.N <= thr) --l0;  // the finest level never joins the tail
-        std::vector<TailLevel<T>> h;
-        size_t arr_off = 0;
-        int elems = 0;
-        // shrink the tail until its levels fit in one CTA's shared memory
+        while (l0 > 1 && lv[l0 - 1].L.N <= thr && lv[l0 - 1].L.n <= nmax) --l0;  // the finest level never joins
+        if (l0 >= nsmooth()) return 0;
+        // shrink the engine until its levels fit in one CTA's shared memory
+        std::vector<TailOp<T>> ops[2];
+        int arr_elems = 0, zero_from = 0, coarse_off = 0, arr_off = 0;
+        size_t smem = 0;
+        const size_t ncf = (size_t)nlu * nlu + 2 * (size_t)nlu;
         for (; l0 < nsmooth(); ++l0) {
-            const int nt = nsmooth() + 1 - l0;
-            h.assign(nt, TailLevel<T>{});
-            elems = 0;
-            for (int i = 0; i < nt; ++i) {
-                const Level<T>& L = lv[l0 + i];
-                const bool coarse = l0 + i == nsmooth();
-                h[i].L = smem_layout(cfg.dim, L.L.N, F);
-                const int a = (int)h[i].L.alloc;
-                auto take = [&](int cnt) { T* p = reinterpret_cast<T*>((size_t)elems); elems += cnt; return p; };
-                h[i].x[0] = take(a);
-                h[i].x[1] = coarse ? h[i].x[0] : take(a);
-                h[i].b = take(a);
-                h[i].r = coarse ? h[i].b : take(a);
-                h[i].sA = L.sA;
-                h[i].sM = L.sM;
+            arr_elems = plan_geometry(l0, F, &zero_from);
+            for (int fz = 0; fz < 2; ++fz) {
+                ops[fz].clear();
+                record(0, fz != 0, ops[fz]);
+                if (int rc = tail_barriers(ops[fz])) return rc;
             }
-            // descriptors + the longest op list (W: every visit is recorded) precede the arrays
-            size_t nops_max = 0;
-            {
-                const int save = tail_l;
-                tail_l = l0;
-                for (int a = 0; a < 2; ++a) {
-                    std::vector<TailOp> ops;
-                    record(l0, a, a == 0, ops);
-                    nops_max = std::max(nops_max, ops.size());
-                }
-                tail_l = save;
-            }
-            arr_off = (nt * sizeof(TailLevel<T>) + nops_max * sizeof(TailOp) + 15) / 16 * 16;
-            const size_t smem = arr_off + ((size_t)elems + nlu) * sizeof(T);
-            if (smem <= (size_t)optin) {
-                tail_smem = smem;
-                break;
-            }
+            const size_t nops = std::max(ops[0].size(), ops[1].size());
+            coarse_off = (int)(nops * sizeof(TailOp<T>));
+            arr_off = (int)((coarse_off + ncf * sizeof(T) + 2 * (size_t)nlu * sizeof(int) + 15) / 16 * 16);
+            smem = arr_off + ((size_t)arr_elems + (nlu > 32 ? nlu : 0)) * sizeof(T);
+            if (smem <= (size_t)optin) break;
         }
         if (l0 >= nsmooth()) return 0;
-        const int nt = nsmooth() + 1 - l0;
-        if (int rc = dalloc(&tail_lv, (size_t)nt)) return rc;
-        CK(cudaMemcpy(tail_lv, h.data(), nt * sizeof(TailLevel<T>), cudaMemcpyHostToDevice));
         tail_l = l0;
-        tail_nlv = nt;
-        tail_elems = elems;
-        tail_arr_off = arr_off;
-        // upload the op lists of every possible entry (buffer a, zero start) now: nothing may
-        // allocate or copy while a cycle is being captured
-        for (int a = 0; a < 2; ++a)
-            for (int fz = 0; fz < 2; ++fz) {
-                std::vector<TailOp> ops;
-                tail_out[a][fz] = record(l0, a, fz != 0, ops);
-                if (int rc = tail_barriers(ops)) return rc;
-                if (int rc = dalloc(&tail_ops[a][fz], ops.size())) return rc;
-                CK(cudaMemcpy(tail_ops[a][fz], ops.data(), ops.size() * sizeof(TailOp), cudaMemcpyHostToDevice));
-                tail_nops[a][fz] = (int)ops.size();
-            }
-        return 0;
-    }
-
-    // the recursion of visit() (multigrid.py:157-185) recorded as tail ops (levels relative to tail_l)
-    // barrier plan of a tail op list: op i waits with the threads of ops i-1 and i; one named
-    // barrier id per distinct thread count (warps skipping small ops run ahead and must not
-    // share a barrier with a different count), id 0 = the whole CTA
-    int tail_barriers(std::vector<TailOp>& ops) {
-        std::vector<int> counts;
-        auto id_of = [&](int n) -> int {
-            if (n >= 1024) return 0;
-            for (size_t k = 0; k < counts.size(); ++k)
-                if (counts[k] == n) return (int)k + 1;
-            counts.push_back(n);
-            return (int)counts.size();
+        for (int fz = 0; fz < 2; ++fz) {
+            if (int rc = dalloc(&tail_ops[fz], ops[fz].size())) return rc;
+            CK(cudaMemcpy(tail_ops[fz], ops[fz].data(), ops[fz].size() * sizeof(TailOp<T>), cudaMemcpyHostToDevice));
+            tail_nops[fz] = (int)ops[fz].size();
+        }
+        // coarse data: -LU off the diagonal, U_jj, 1/U_jj (correctly rounded host division);
+        // the row interchanges of getrs (laswp) folded into a gather order
+        std::vector<T> cf(ncf);
+        for (int i = 0; i < nlu; ++i)
+            for (int j = 0; j < nlu; ++j) cf[(size_t)i * nlu + j] = i == j ? T(0) : (T)(-lu_h[(size_t)i * nlu + j]);
+        for (int j = 0; j < nlu; ++j) {
+            const T d = (T)lu_h[(size_t)j * nlu + j];
+            cf[(size_t)nlu * nlu + j] = d;
+            cf[(size_t)nlu * nlu + nlu + j] = T(1) / d;
+        }
+        std::vector<int> perm(nlu), ci(2 * (size_t)nlu);
+        for (int i = 0; i < nlu; ++i) perm[i] = i;
+        for (int i = 0; i < nlu; ++i) std::swap(perm[i], perm[piv_h[i]]);
+        const TGeo& cg = tg.back();
+        auto off = [&](int q) {
+            const int n = cg.n;
+            if (cfg.dim == 2) return (q / n) * cg.s0 + q % n;
+            return (q / (n * n)) * cg.s0 + ((q / n) % n) * cg.s1 + q % n;
         };
-        int prev = 1024;
-        for (TailOp& op : ops) {
-            op.npre = std::max(op.nthr, prev);
-            prev = op.nthr;
-            op.bid_pre = id_of(op.npre);
-            op.bid_in = id_of(op.nthr);
+        for (int i = 0; i < nlu; ++i) {
+            ci[i] = off(perm[i]);
+            ci[nlu + i] = off(i);
         }
-        if (counts.size() > 15) return fail(SPAIMG_ENOTSUP, "tail: too many distinct level sizes for named barriers");
-        return 0;
-    }
-
-    // threads of a tail op on level l: one per point, whole warps, at most one CTA
-    int tail_threads(int l) const {
-        const long long cnt = count_of(cfg.dim, lv[l].L.N);
-        return (int)std::min<long long>(1024, (cnt + 31) / 32 * 32);
-    }
-
-    int record(int l, int a, bool fz, std::vector<TailOp>& ops) {
-        const int rl = l - tail_l;
-        const int nt = tail_threads(l);
-        const int nt_coarse = nlu <= 32 ? 32 : (int)std::min(1024, (nlu + 31) / 32 * 32);
-        if (l == nsmooth()) {
-            ops.push_back(TailOp{TAIL_COARSE, rl, 0, 0, 0, 0, nt_coarse});
-            return 0;
-        }
-        for (int k = 0; k < cfg.nu1; ++k) {
-            ops.push_back(TailOp{TAIL_SWEEP, rl, a, 1 - a, 0, fz ? 1 : 0, nt});
-            a = 1 - a;
-            fz = false;
-        }
-        if (fz) ops.push_back(TailOp{TAIL_ZERO, rl, a, a, 0, 0, nt});
-        ops.push_back(TailOp{TAIL_RESTRICT, rl, a, a, 0, 0, nt});
-        int c;
-        if (l + 1 == nsmooth()) {
-            ops.push_back(TailOp{TAIL_COARSE, rl + 1, 0, 0, 0, 0, nt_coarse});
-            c = 0;
-        } else {
-            c = record(l + 1, 0, true, ops);
-            for (int g = 1; g < cfg.gamma; ++g) c = record(l + 1, c, false, ops);
-        }
-        ops.push_back(TailOp{TAIL_PROLONG, rl, a, a, c, 0, nt});
-        for (int k = 0; k < cfg.nu2; ++k) {
-            ops.push_back(TailOp{TAIL_SWEEP, rl, a, 1 - a, 0, 0, nt});
-            a = 1 - a;
-        }
-        return a;
-    }
-
-    TailArgs<T> make_tail_args(int a, int z) const {
-        const Level<T>& G = lv[tail_l];
-        TailArgs<T> ta{};
-        ta.lv = tail_lv;
-        ta.ops = tail_ops[a][z];
-        ta.nlv = tail_nlv;
-        ta.nops = tail_nops[a][z];
-        ta.arr_off = tail_arr_off;
-        ta.arr_elems = tail_elems;
-        ta.smem = tail_smem;
+        if (int rc = dalloc(&tail_coarse, ncf)) return rc;
+        CK(cudaMemcpy(tail_coarse, cf.data(), ncf * sizeof(T), cudaMemcpyHostToDevice));
+        if (int rc = dalloc(&tail_coarse_idx, ci.size())) return rc;
+        CK(cudaMemcpy(tail_coarse_idx, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
+        TailArgs<T>& ta = tail_args;
+        ta.coarse = tail_coarse;
+        ta.coarse_idx = tail_coarse_idx;
+        ta.nlu = nlu;
+        ta.coarse_off = coarse_off;
+        ta.arr_off = arr_off;
+        ta.arr_elems = arr_elems;
+        ta.zero_from = zero_from;
+        ta.smem = smem;
         ta.M = M;
         ta.omega = omega;
-        ta.lu = lu;
-        ta.piv = piv;
-        ta.nlu = nlu;
-        ta.gL = G.L;
-        ta.gb = G.b;
-        ta.gx_in = G.x[a];
-        ta.out_a = tail_out[a][z];
-        ta.gx_out = G.x[ta.out_a];
-        ta.entry_fz = z;
+        ta.gL = lv[l0].L;
+        ta.frame = F;
+        ta.e_s0 = tg[0].s0;
+        ta.e_s1 = tg[0].s1;
+        ta.e_x = tg[0].x;
+        ta.e_b = tg[0].b;
         ta.shape = shape;
-        ta.entry_a = a;
-        return ta;
-    }
-
-    int tail_visit(int l, int a, bool fz, cudaStream_t s, int* launches) {
-        if (l != tail_l) return -1;
-        const TailArgs<T> ta = make_tail_args(a, fz ? 1 : 0);
-        if (launch_tail<T>(ta, s) != cudaSuccess) return -1;
-        ++*launches;
-        return ta.out_a;
-    }
-
-    // ---- cluster tail: levels cl_l .. tail_l-1 on a thread-block cluster, then the solo tail --
-    // opt-in (SPAIMG_CLUSTER_N): bitwise correct, but measured slower than the per-op kernels at
-    // every threshold (c1 +14 %, c2 +3 %, c3 2x at N<=64): point-parallel phases over L2 with a
-    // cluster barrier each lose to the shared-memory tiles of the flat kernels
-    static int cluster_threshold(const spaimg_mg_config&) {
-        const char* e = getenv("SPAIMG_CLUSTER_N");
-        return e ? atoi(e) : 0;
-    }
-    int cl_l = 1 << 30;
-    int cl_size = 16;
-    TailLevel<T>* cl_lv = nullptr;
-    TailOp* cl_ops[2][2] = {};
-    int cl_nops[2][2] = {};
-    int cl_out[2][2] = {};
-
-    int record_cluster(int l, int a, bool fz, std::vector<TailOp>& ops) {
-        const int rl = l - cl_l;
-        if (l == tail_l) {
-            ops.push_back(TailOp{TAIL_SOLO, rl, a, 0, 0, fz ? 1 : 0, 0, 0, 0, 0});
-            return tail_out[a][fz ? 1 : 0];
-        }
-        for (int k = 0; k < cfg.nu1; ++k) {
-            ops.push_back(TailOp{TAIL_SWEEP, rl, a, 1 - a, 0, fz ? 1 : 0, 0, 0, 0, 0});
-            a = 1 - a;
-            fz = false;
-        }
-        if (fz) ops.push_back(TailOp{TAIL_ZERO, rl, a, a, 0, 0, 0, 0, 0, 0});
-        ops.push_back(TailOp{TAIL_RESTRICT, rl, a, a, 0, 0, 0, 0, 0, 0});
-        int c = record_cluster(l + 1, 0, true, ops);
-        for (int g = 1; g < cfg.gamma; ++g) c = record_cluster(l + 1, c, false, ops);
-        ops.push_back(TailOp{TAIL_PROLONG, rl, a, a, c, 0, 0, 0, 0, 0});
-        for (int k = 0; k < cfg.nu2; ++k) {
-            ops.push_back(TailOp{TAIL_SWEEP, rl, a, 1 - a, 0, 0, 0, 0, 0, 0});
-            a = 1 - a;
-        }
-        return a;
-    }
-
-    int init_cluster() {
-        const int thr = cluster_threshold(cfg);
-        if (thr <= 0 || tail_l >= nsmooth() || !fused) return 0;
-        int l0 = tail_l;
-        while (l0 > 1 && lv[l0 - 1].L.N <= thr) --l0;
-        if (l0 >= tail_l) return 0;
-        // a 16-CTA cluster where the device allows one, else 8
-        {
-            int ncl = 0;
-            cl_size = cluster_occupancy<T>(16, tail_smem, &ncl) == cudaSuccess && ncl > 0 ? 16 : 8;
-        }
-        const int nt = tail_l + 1 - l0;
-        std::vector<TailLevel<T>> h(nt);
-        for (int i = 0; i < nt; ++i) {
-            const Level<T>& L = lv[l0 + i];
-            h[i].L = L.L;
-            h[i].x[0] = L.x[0];
-            h[i].x[1] = L.x[1];
-            h[i].b = L.b;
-            h[i].r = L.r;
-            h[i].sA = L.sA;
-            h[i].sM = L.sM;
-            if (i < nt - 1 && !L.r) return 0;  // needs the level's scratch r
-        }
-        if (int rc = dalloc(&cl_lv, (size_t)nt)) return rc;
-        CK(cudaMemcpy(cl_lv, h.data(), nt * sizeof(TailLevel<T>), cudaMemcpyHostToDevice));
-        cl_l = l0;
-        for (int a = 0; a < 2; ++a)
-            for (int fz = 0; fz < 2; ++fz) {
-                std::vector<TailOp> ops;
-                cl_out[a][fz] = record_cluster(l0, a, fz != 0, ops);
-                if (int rc = dalloc(&cl_ops[a][fz], ops.size())) return rc;
-                CK(cudaMemcpy(cl_ops[a][fz], ops.data(), ops.size() * sizeof(TailOp), cudaMemcpyHostToDevice));
-                cl_nops[a][fz] = (int)ops.size();
-            }
         return 0;
     }
 
-    int cluster_visit(int a, bool fz, cudaStream_t s, int* launches) {
+    // one visit of the engine's entry level: x[a] updated in place
+    int tail_visit(int l, int a, bool fz, cudaStream_t s, int* launches) {
+        if (l != tail_l) return -1;
+        TailArgs<T> ta = tail_args;
         const int z = fz ? 1 : 0;
-        ClusterArgs<T> ca{};
-        ca.lv = cl_lv;
-        ca.ops = cl_ops[a][z];
-        ca.nops = cl_nops[a][z];
-        ca.M = M;
-        ca.omega = omega;
-        for (int i = 0; i < 2; ++i)
-            for (int j = 0; j < 2; ++j) ca.solo[i][j] = make_tail_args(i, j);
-        if (launch_cluster_tail<T>(ca, cl_size, tail_smem, s) != cudaSuccess) return -1;
+        ta.ops = tail_ops[z];
+        ta.nops = tail_nops[z];
+        ta.gb = lv[l].b;
+        ta.gx = lv[l].x[a];
+        if (launch_tail<T>(ta, s) != cudaSuccess) return -1;
         ++*launches;
-        return cl_out[a][z];
+        return a;
     }
 
     // ||b - A x||_2 of the finest level appended to the device history
     int norm_launch(const T* x, cudaStream_t s, int* launches) {
         const Level<T>& L = lv[0];
-        if (sweep_norm_supported()) {
-            CK(launch_norm_march<T>(L.L, x, L.b, L.sA, fold_check ? norm_sink_cond(cur_cond) : norm_sink(), s));
-        } else {
-            CK(launch_residual_norm<T>(L.L, x, L.b, L.sA, partials, counter, norms_d, 0, slot_d, s));
-        }
+        CK(launch_norm_march<T>(L.L, x, L.b, L.sA, in_solve_graph ? norm_sink_cond(cur_cond) : norm_sink(), s));
         ++*launches;
         return 0;
     }
 
-    static bool rrfz_enabled(int dim) {
-        const char* e = getenv("SPAIMG_RRFZ");
-        if (e) return e[0] == '1';
-        return dim == 2;
-    }
-
     // recursive schedule (multigrid.py:157-185).  Returns the buffer index of level l holding
     // the result, or -1 on error.  pre_done: the first pre-sweep already ran (level 0: part A;
-    // small levels: fused into the finer level's residual + restriction kernel).
-    int visit(int l, int a, bool fz, cudaStream_t s, int* launches, bool pre_done, bool rr_done = false) {
-        if (l == cl_l) return cluster_visit(a, fz, s, launches);
+    // small 2D levels: fused into the finer level's residual + restriction kernel).
+    int visit(int l, int a, bool fz, cudaStream_t s, int* launches, bool pre_done) {
         if (l >= tail_l && l < nsmooth()) return tail_visit(l, a, fz, s, launches);
         Level<T>& L = lv[l];
         if (l == nsmooth()) {  // u.N <= coarsest_N: direct solve (multigrid.py:166-167)
@@ -876,21 +835,9 @@ template <class T> struct Solver final : spaimg_solver {
             ++*launches;
             return 0;
         }
-        Level<T>& C0 = lv[l + 1];
-        // the last pre-sweep of a 2D marching level carries the residual + restriction (K1+K2)
-        const bool pr = !rr_done && fused && cfg.nu1 >= 1 && sweep_rr_supported(L.L);
         for (int k = 0; k < cfg.nu1; ++k) {
-            if (!(pre_done && k == 0)) {
-                if (pr && k == cfg.nu1 - 1) {
-                    if (launch_sweep_rr<T>(L.L, C0.L, L.x[a], L.b, L.x[1 - a], C0.b, M, shape, L.sA, L.sM, omega, fz, s,
-                                           nullptr) != cudaSuccess)
-                        return -1;
-                    ++*launches;
-                    rr_done = true;
-                } else if (do_sweep<T>(L, a, fz, M, shape, fused, omega, s, launches)) {
-                    return -1;
-                }
-            }
+            if (!(pre_done && k == 0))
+                if (do_sweep<T>(L, a, fz, M, shape, fused, omega, s, launches)) return -1;
             a = 1 - a;
             fz = false;
         }
@@ -901,20 +848,17 @@ template <class T> struct Solver final : spaimg_solver {
         Level<T>& C = lv[l + 1];
         // on the small 2D levels the coarse level's first (zero-start) pre-sweep rides with K2
         // (measured: c2 -1.7 %, c1 -3.5 %; in 3D the ring recomputation costs more than the
-        // launch it saves, c3 +7 %, so 3D keeps two kernels unless SPAIMG_RRFZ=1)
-        const bool rr_fz = !rr_done && fused && cfg.nu1 >= 1 && l + 1 < nsmooth() && l + 1 < std::min(tail_l, cl_l) &&
-                           L.L.N <= flat_threshold(cfg.dim) && !getenv("SPAIMG_RESTRICT_V1") && rrfz_enabled(cfg.dim);
-        if (rr_done) {
-            // C.b came with the last pre-sweep
-        } else if (rr_fz) {
+        // launch it saves, c3 +7 %, so 3D keeps two kernels)
+        const bool rr_fz = fused && cfg.nu1 >= 1 && l + 1 < nsmooth() && l + 1 < tail_l &&
+                           L.L.N <= flat_threshold(cfg.dim) && cfg.dim == 2;
+        if (rr_fz) {
             if (launch_residual_restrict_fz<T>(L.L, C.L, L.x[a], L.b, C.b, C.x[1], M, shape, L.sA, C.sM, omega, s) !=
                 cudaSuccess)
                 return -1;
-            ++*launches;
         } else {
-            if (launch_residual_restrict<T>(L.L, C.L, L.x[a], L.b, C.b, L.sA, L.r, s) != cudaSuccess) return -1;
-            *launches += residual_restrict_launches(cfg.dim);
+            if (launch_residual_restrict<T>(L.L, C.L, L.x[a], L.b, C.b, L.sA, s) != cudaSuccess) return -1;
         }
+        ++*launches;
         int c;
         if (l + 1 == nsmooth()) {
             if (launch_coarse_solve<T>(C.L, C.b, C.x[0], lu, piv, nlu, s) != cudaSuccess) return -1;
@@ -953,13 +897,7 @@ template <class T> struct Solver final : spaimg_solver {
     int part_a(cudaStream_t s, int* launches) {
         if (fused_norm) {
             Level<T>& L = lv[0];
-            const NormOut no = fold_check ? norm_sink_cond(cur_cond) : norm_sink();
-            if (a_rr) {  // norm + first (only) pre-sweep + residual + restriction in one march
-                CK(launch_sweep_rr<T>(L.L, lv[1].L, L.x[0], L.b, L.x[1], lv[1].b, M, shape, L.sA, L.sM, omega, false, s,
-                                      &no));
-                ++*launches;
-                return 0;
-            }
+            const NormOut no = in_solve_graph ? norm_sink_cond(cur_cond) : norm_sink();
             CK(launch_sweep<T>(L.L, L.x[0], L.b, L.x[1], M, shape, L.sA, L.sM, omega, false, s, &no));
             ++*launches;
             return 0;
@@ -969,7 +907,7 @@ template <class T> struct Solver final : spaimg_solver {
 
     // B: the rest of the cycle; ends with the iterate back in x[0]
     int part_b(cudaStream_t s, int* launches) {
-        const int out = visit(0, 0, false, s, launches, fused_norm, a_rr);
+        const int out = visit(0, 0, false, s, launches, fused_norm);
         if (out != 0) return fail(SPAIMG_EINVAL, out < 0 ? "cycle launch failed: " + g_err : "cycle parity error");
         return 0;
     }
@@ -1011,13 +949,8 @@ template <class T> struct Solver final : spaimg_solver {
         return 0;
     }
 
-    // reset; A; check; WHILE(cont) { B; A; check }.  A (norm of u_k fused with the first
-    // pre-sweep of cycle k+1, which only writes the other buffer) is harmlessly speculative
-    // when the check then stops, so no IF node is needed around B (SPAIMG_SOLVE_IF=1 keeps the
-    // reset; WHILE { A; check; IF { B } } form for comparison).
+    // reset; A; WHILE(cont) { B; A }  (see the comment above k_solve_reset)
     int build_solve_graph() {
-        const char* ef = getenv("SPAIMG_SOLVE_IF");
-        if (ef && ef[0] == '1') return build_solve_graph_if();
         cudaGraph_t g;
         CK(cudaGraphCreate(&g, 0));
         int launches_a = 0, launches_b = 0, dummy = 0;
@@ -1026,68 +959,20 @@ template <class T> struct Solver final : spaimg_solver {
         int rc = 0;
         cudaError_t e = cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault);
         if (e != cudaSuccess) rc = fail((int)e, "conditional handle");
-        // the stop test rides in the norm's last CTA (no separate check node) when the norm
-        // comes from the marching kernels (SPAIMG_FOLD_CHECK=0 keeps the check kernel)
-        const char* ef2 = getenv("SPAIMG_FOLD_CHECK");
-        fold_check = sweep_norm_supported() && !(ef2 && ef2[0] == '0');
+        in_solve_graph = true;
         cur_cond = hw;
         if (!rc)
             rc = capture_into(g, [&](cudaStream_t cs) -> int {
-                CK(launch_pdl(k_solve_reset, dim3(1), dim3(1), 0, cs, slot_d, state_d));
+                CK(launch_k(k_solve_reset, dim3(1), dim3(1), 0, cs, slot_d, state_d));
                 if (int r = part_a(cs, &dummy)) return r;
-                if (!fold_check)
-                    CK(launch_pdl(k_solve_check, dim3(1), dim3(1), 0, cs, norms_d, slot_d, ctl_d, state_d, hw, hw));
                 return add_conditional(cs, hw, cudaGraphCondTypeWhile, &wbody);
             });
         if (!rc)
             rc = capture_into(wbody, [&](cudaStream_t cs) -> int {
                 if (int r = part_b(cs, &launches_b)) return r;
-                if (int r = part_a(cs, &launches_a)) return r;
-                if (!fold_check) {
-                    CK(launch_pdl(k_solve_check, dim3(1), dim3(1), 0, cs, norms_d, slot_d, ctl_d, state_d, hw, hw));
-                    ++launches_a;
-                }
-                return 0;
+                return part_a(cs, &launches_a);
             });
-        fold_check = false;
-        if (!rc) {
-            e = cudaGraphInstantiate(&exec_solve, g, 0);
-            if (e != cudaSuccess) rc = fail((int)e, std::string("solve graph instantiate: ") + cudaGetErrorString(e));
-        }
-        cudaGraphDestroy(g);
-        if (!rc) {
-            kernels_per_cycle = launches_a + launches_b;
-            kernels_a = launches_a;
-        }
-        return rc;
-    }
-
-    int build_solve_graph_if() {
-        cudaGraph_t g;
-        CK(cudaGraphCreate(&g, 0));
-        int launches_a = 0, launches_b = 0;
-        cudaGraphConditionalHandle hw, hi;
-        cudaGraph_t wbody = nullptr, ibody = nullptr;
-        int rc = 0;
-        cudaError_t e = cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault);
-        if (e != cudaSuccess) rc = fail((int)e, "conditional handle");
-        if (!rc)
-            rc = capture_into(g, [&](cudaStream_t cs) -> int {
-                CK(launch_pdl(k_solve_reset, dim3(1), dim3(1), 0, cs, slot_d, state_d));
-                return add_conditional(cs, hw, cudaGraphCondTypeWhile, &wbody);
-            });
-        if (!rc) {
-            e = cudaGraphConditionalHandleCreate(&hi, wbody, 0, cudaGraphCondAssignDefault);
-            if (e != cudaSuccess) rc = fail((int)e, "conditional handle (if)");
-        }
-        if (!rc)
-            rc = capture_into(wbody, [&](cudaStream_t cs) -> int {
-                if (int r = part_a(cs, &launches_a)) return r;
-                CK(launch_pdl(k_solve_check, dim3(1), dim3(1), 0, cs, norms_d, slot_d, ctl_d, state_d, hw, hi));
-                ++launches_a;
-                return add_conditional(cs, hi, cudaGraphCondTypeIf, &ibody);
-            });
-        if (!rc) rc = capture_into(ibody, [&](cudaStream_t cs) -> int { return part_b(cs, &launches_b); });
+        in_solve_graph = false;
         if (!rc) {
             e = cudaGraphInstantiate(&exec_solve, g, 0);
             if (e != cudaSuccess) rc = fail((int)e, std::string("solve graph instantiate: ") + cudaGetErrorString(e));
@@ -1116,7 +1001,6 @@ template <class T> struct Solver final : spaimg_solver {
         cudaGraphDestroy(g);
         return rc;
     }
-
     int load(const void* b, const void* u0, cudaStream_t s) override {
         Scratch sc(s);
         Level<T>& L = lv[0];
@@ -1128,11 +1012,18 @@ template <class T> struct Solver final : spaimg_solver {
             CK(cudaMemsetAsync(L.x[0], 0, (size_t)L.L.alloc * sizeof(T), s));
         }
         CK(cudaMemsetAsync(slot_d, 0, sizeof(int), s));
+        hist_len = 0;
         return 0;
     }
 
-    // n full cycles (each appends its residual norm to the device history)
+    // norms appended to the device history since the last reset of its cursor (load / run)
+    long long hist_len = 0;
+
+    // n full cycles (each appends its residual norm to the device history, grown as needed)
     int cycles(int n, cudaStream_t s) override {
+        if (hist_len + n > (1LL << 24)) return fail(SPAIMG_EINVAL, "too many cycles without a reload");
+        if (int rc = grow_norms((int)(hist_len + n))) return rc;
+        hist_len += n;
         if (use_graph && !exec_cycle)
             if (int rc = build_cycle_graph()) return rc;
         for (int k = 0; k < n; ++k) {
@@ -1148,7 +1039,8 @@ template <class T> struct Solver final : spaimg_solver {
     }
 
     int run(double tol, int max_iters, double* norms, int* iters, int* conv, cudaStream_t s) override {
-        if (max_iters + 1 > norms_cap) return fail(SPAIMG_EINVAL, "max_iters too large");
+        if (int rc = grow_norms(max_iters + 1)) return rc;
+        hist_len = 0;
         if (!use_graph) return run_host_loop(tol, max_iters, norms, iters, conv, s);
         if (!exec_solve)
             if (int rc = build_solve_graph()) return rc;
@@ -1230,7 +1122,8 @@ template <class T> struct Solver final : spaimg_solver {
 
     int solve_batch(int nrhs, const void* const* bh, void* const* uh, double tol, int max_iters, double* norms,
                     int* iters, int* conv, cudaStream_t s) override {
-        if (max_iters + 1 > norms_cap) return fail(SPAIMG_EINVAL, "max_iters too large");
+        if (int rc = grow_norms(max_iters + 1)) return rc;
+        hist_len = 0;
         if (nrhs <= 0) return 0;
         if (!use_graph) return fail(SPAIMG_ENOTSUP, "solve_batch needs the graph path");
         if (!exec_solve)
@@ -1245,13 +1138,14 @@ template <class T> struct Solver final : spaimg_solver {
         CK(cudaEventRecord(ev_go, s));
         CK(cudaStreamWaitEvent(bs_h2d, ev_go, 0));
         CK(cudaStreamWaitEvent(bs_d2h, ev_go, 0));
-        CK(cudaMemcpyAsync(bstage_in[0], bh[0], bytes, cudaMemcpyHostToDevice, bs_h2d));
+        // cudaMemcpyDefault: the right-hand sides and outputs may be host or device arrays
+        CK(cudaMemcpyAsync(bstage_in[0], bh[0], bytes, cudaMemcpyDefault, bs_h2d));
         CK(cudaEventRecord(ev_in[0], bs_h2d));
         for (int i = 0; i < nrhs; ++i) {
             const int c = i & 1, o = c ^ 1;
             if (i + 1 < nrhs) {  // prefetch the next right-hand side once its stage is free
                 if (i >= 1) CK(cudaStreamWaitEvent(bs_h2d, ev_pad[o], 0));
-                CK(cudaMemcpyAsync(bstage_in[o], bh[i + 1], bytes, cudaMemcpyHostToDevice, bs_h2d));
+                CK(cudaMemcpyAsync(bstage_in[o], bh[i + 1], bytes, cudaMemcpyDefault, bs_h2d));
                 CK(cudaEventRecord(ev_in[o], bs_h2d));
             }
             CK(cudaStreamWaitEvent(s, ev_in[c], 0));
@@ -1267,7 +1161,7 @@ template <class T> struct Solver final : spaimg_solver {
             CK(launch_unpad<T>(L0.L, L0.x[0], bstage_out[c], s));
             CK(cudaEventRecord(ev_unpad[c], s));
             CK(cudaStreamWaitEvent(bs_d2h, ev_unpad[c], 0));
-            CK(cudaMemcpyAsync(uh[i], bstage_out[c], bytes, cudaMemcpyDeviceToHost, bs_d2h));
+            CK(cudaMemcpyAsync(uh[i], bstage_out[c], bytes, cudaMemcpyDefault, bs_d2h));
             CK(cudaEventRecord(ev_out[c], bs_d2h));
         }
         CK(cudaStreamWaitEvent(s, ev_out[(nrhs - 1) & 1], 0));
@@ -1289,7 +1183,7 @@ template <class T> struct Solver final : spaimg_solver {
         int launches = 0;
         switch (which) {
             case 0: return do_sweep<T>(L, 0, false, M, shape, fused, omega, s, nullptr);
-            case 1: CK(launch_residual_restrict<T>(L.L, lv[1].L, L.x[0], L.b, lv[1].b, L.sA, L.r, s)); return 0;
+            case 1: CK(launch_residual_restrict<T>(L.L, lv[1].L, L.x[0], L.b, lv[1].b, L.sA, s)); return 0;
             case 2: CK(launch_prolong_correct<T>(L.L, lv[1].L, L.x[1], L.x[1], lv[1].x[0], s)); return 0;
             case 3: {
                 // keep the history cursor in range while timing repeated norms

@@ -32,14 +32,6 @@ template <> struct Op<float> {
 };
 
 // ------------------------------------------------------------------------------------------
-// Programmatic Dependent Launch (sm_90+): every cycle-path kernel waits for its predecessor
-// grid before touching memory and lets its dependent launch as its own CTAs finish, so a
-// dependent kernel's launch latency overlaps the primary's tail.
-// ------------------------------------------------------------------------------------------
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-
-// ------------------------------------------------------------------------------------------
 // padded level layout ("ghost frame"): every level of the hierarchy lives in a zero-framed,
 // pitched array so that stencil loads never need bounds checks (the frame IS the reference's
 // zero extension, stencils.py:139-146) and every row starts 128-byte aligned.

@@ -9,6 +9,7 @@ tests only ever read them.
     python tests/golden/make_golden.py hist c1 c3   # residual histories (zero u0)
     python tests/golden/make_golden.py hist c2      # ~5 min of CPU
     python tests/golden/make_golden.py hist c4      # ~1 h of CPU, ~10 GB RSS
+    python tests/golden/make_golden.py hist c1 c3 c2 --only "W("   # the W(1,0) defaults only
 
 The zero-u0 history loop below is the harness SURVEY.md Finding 2 describes:
 it calls the reference `cycle()` and repeats `solve()`'s norm and stop logic
@@ -59,12 +60,21 @@ def rhs_for(cfg_id: str) -> Grid:
     raise KeyError(cfg_id)
 
 
+# (smoother, nu1, nu2[, cycle, coarsest_N]); the 3-tuples are V-cycles with coarsest_N = 2.
+# The W(1,0), coarsest_N = 4 runs are the reference MgConfig defaults (multigrid.py:39-43).
 RUNS = {
-    "c1": [("m9", 1, 1)],
-    "c3": [("m7", 1, 1)],
-    "c2": [("m9", 1, 1), ("m9", 2, 2), ("jacobi2d", 1, 1), ("jacobi2d", 2, 2)],
-    "c4": [("m7", 1, 1), ("m7", 2, 2), ("jacobi3d", 1, 1), ("jacobi3d", 2, 2)],
+    "c1": [("m9", 1, 1), ("m9", 1, 0, "W", 4)],
+    "c3": [("m7", 1, 1), ("m7", 1, 0, "W", 4)],
+    "c2": [("m9", 1, 1), ("m9", 2, 2), ("jacobi2d", 1, 1), ("jacobi2d", 2, 2), ("m9", 1, 0, "W", 4)],
+    "c4": [("m7", 1, 1), ("m7", 2, 2), ("jacobi3d", 1, 1), ("jacobi3d", 2, 2), ("m7", 1, 0, "W", 4)],
 }
+
+
+def run_key(cid, run):
+    sm, nu1, nu2 = run[:3]
+    cyc, nc = (run[3], run[4]) if len(run) > 3 else ("V", 2)
+    key = f"{cid}/{sm}/{cyc}({nu1},{nu2})"
+    return (key if (cyc, nc) == ("V", 2) else f"{key}/cN{nc}"), sm, nu1, nu2, cyc, nc
 
 
 def zero_start_history(b: Grid, cfg: MgConfig):
@@ -92,18 +102,20 @@ def zero_start_history(b: Grid, cfg: MgConfig):
                    s_per_cycle=wall / k, wall_s=wall)
 
 
-def cmd_hist(cfg_ids):
+def cmd_hist(cfg_ids, only=None):
     path = os.path.join(HERE, "histories.json")
     data = json.load(open(path)) if os.path.exists(path) else {}
     for cid in cfg_ids:
         b = rhs_for(cid)
-        for sm, nu1, nu2 in RUNS[cid]:
-            key = f"{cid}/{sm}/V({nu1},{nu2})"
-            cfg = MgConfig(smoother=named(sm), cycle="V", nu1=nu1, nu2=nu2,
-                           coarsest_N=2, tol=1e-10, max_iters=100)
+        for run in RUNS[cid]:
+            key, sm, nu1, nu2, cyc, nc = run_key(cid, run)
+            if only and only not in key:
+                continue
+            cfg = MgConfig(smoother=named(sm), cycle=cyc, nu1=nu1, nu2=nu2,
+                           coarsest_N=nc, tol=1e-10, max_iters=100)
             _, rec = zero_start_history(b, cfg)
-            rec.update(config=cid, smoother=sm, nu1=nu1, nu2=nu2, cycle="V",
-                       coarsest_N=2, tol=1e-10, N=b.N, dim=b.dim, sha_b=sha(b.values),
+            rec.update(config=cid, smoother=sm, nu1=nu1, nu2=nu2, cycle=cyc,
+                       coarsest_N=nc, tol=1e-10, N=b.N, dim=b.dim, sha_b=sha(b.values),
                        host_cpu=_cpu_model(), numpy=np.__version__)
             data[key] = rec
             print(key, rec["iterations"], rec["norms"][-1], f"{rec['s_per_cycle']:.3f} s/cycle",
@@ -207,6 +219,13 @@ if __name__ == "__main__":
     if sys.argv[1] == "ops":
         cmd_ops()
     elif sys.argv[1] == "hist":
-        cmd_hist(sys.argv[2:])
+        # optional trailing "--only <substring>" selects runs by key, e.g. --only W(
+        args = sys.argv[2:]
+        only = None
+        if "--only" in args:
+            i = args.index("--only")
+            only = args[i + 1]
+            args = args[:i] + args[i + 2:]
+        cmd_hist(args, only)
     else:
         raise SystemExit(__doc__)

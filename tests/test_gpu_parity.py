@@ -108,10 +108,10 @@ def test_default_solve_vs_reference_golden(golden_meta, side):
         assert rep.rho_hat == pytest.approx(rec["rho_hat"], rel=1e-8)
 
 
-def _zero_start(cfg_id, sm, nu1, nu2, side="device"):
+def _zero_start(cfg_id, sm, nu1, nu2, side="device", cycle="V", coarsest_N=2):
     b = workloads.rhs(cfg_id)
     dim, N, _ = workloads.CONFIGS[cfg_id]
-    cfg = sp.MgConfig(smoother=sp.named(sm), cycle="V", nu1=nu1, nu2=nu2, coarsest_N=2)
+    cfg = sp.MgConfig(smoother=sp.named(sm), cycle=cycle, nu1=nu1, nu2=nu2, coarsest_N=coarsest_N)
     bg = sp.Grid(N, dev(b) if side == "device" else b)
     u, rep = sp.solve(bg, cfg, u0=0)
     return b, u, rep
@@ -136,17 +136,19 @@ def test_small_configs_histories(golden_hist, cfg_id, sm):
 
 
 @pytest.mark.parametrize("key", ["c2/m9/V(1,1)", "c2/m9/V(2,2)", "c2/jacobi2d/V(1,1)", "c2/jacobi2d/V(2,2)",
-                                 "c4/m7/V(1,1)", "c4/m7/V(2,2)", "c4/jacobi3d/V(1,1)", "c4/jacobi3d/V(2,2)"])
+                                 "c4/m7/V(1,1)", "c4/m7/V(2,2)", "c4/jacobi3d/V(1,1)", "c4/jacobi3d/V(2,2)",
+                                 "c1/m9/W(1,0)/cN4", "c3/m7/W(1,0)/cN4", "c2/m9/W(1,0)/cN4", "c4/m7/W(1,0)/cN4"])
 def test_large_configs_vs_reference_golden(golden_hist, key):
-    """Configs 2 and 4 at full size against the reference's own histories (generated in the
-    build container, tests/golden/histories.json): identical cycle counts, histories within
-    1e-8 relative, and the final iterate bitwise (sha256)."""
+    """Configs 1-4 at full size against the reference's own histories (generated in the build
+    container, tests/golden/histories.json): identical cycle counts, histories within 1e-8
+    relative, and the final iterate bitwise (sha256).  The W(1,0), coarsest_N = 4 runs are the
+    reference MgConfig defaults (multigrid.py:39-43)."""
     if key not in golden_hist:
         pytest.skip(f"golden history {key} not generated yet")
     rec = golden_hist[key]
-    cfg_id, sm, v = key.split("/")
+    cfg_id, sm, v = key.split("/")[:3]
     nu1, nu2 = int(v[2]), int(v[4])
-    b, u, rep = _zero_start(cfg_id, sm, nu1, nu2)
+    b, u, rep = _zero_start(cfg_id, sm, nu1, nu2, cycle=rec["cycle"], coarsest_N=rec["coarsest_N"])
     assert hashlib.sha256(b.tobytes()).hexdigest() == rec["sha_b"]
     assert rep.iterations == rec["iterations"] and rep.converged
     rel = max(abs(a - r) / r for a, r in zip(rep.residual_norms, rec["norms"]))
@@ -256,35 +258,30 @@ def test_solve_batch_pipelined_matches_single_solves(dim, N, sm):
         assert np.array_equal(u.numpy(), ref_u.values)
 
 
-@pytest.mark.parametrize("env", [{"SPAIMG_NO_GRAPH": "1"}, {"SPAIMG_RESTRICT_V1": "1"}, {"SPAIMG_SWEEP_V1": "1"},
-                                 {"SPAIMG_PDL": "1"}, {"SPAIMG_PC_FLAT": "1"}, {"SPAIMG_TAIL_N": "0"},
-                                 {"SPAIMG_FOLD_CHECK": "0"}, {"SPAIMG_SOLVE_IF": "1"}, {"SPAIMG_RRFZ": "0"}, {"SPAIMG_RRFZ": "1"},
-                                 {"SPAIMG_PR": "1"}, {"SPAIMG_PR": "1", "SPAIMG_FLAT_N2": "0"}, {"SPAIMG_CLUSTER_N": "64"},
-                                 {"SPAIMG_CLUSTER_N": "1024"},
-                                 {"SPAIMG_FLAT_N2": "0", "SPAIMG_FLAT_N3": "0", "SPAIMG_PC": "0"}],
-                         ids=lambda e: ",".join(f"{k[7:]}={v}" for k, v in e.items()))
+@pytest.mark.parametrize("env", [{}, {"SPAIMG_NO_GRAPH": "1"}, {"SPAIMG_TAIL_N": "0"}, {"SPAIMG_TAIL_N": "8"},
+                                 {"SPAIMG_TAIL_N": "32"}, {"SPAIMG_FLAT_N2": "0", "SPAIMG_FLAT_N3": "0"}],
+                         ids=lambda e: ",".join(f"{k[7:]}={v}" for k, v in e.items()) or "default")
 def test_alternate_paths_bitwise(env):
-    """Every opt-in / fallback kernel path (eager launches, unfused restriction, v1 tile sweeps,
-    PDL, flat K3+K1 fusion, no tail kernel, marching on every level without K3 fusion) gives
-    the same iterations, histories and bitwise iterates as the C oracle."""
+    """The default schedule and every tuning switch (eager launches; the shared-memory coarse
+    engine off or entered at other sizes; marching kernels on every level) give the same
+    iterations, histories and bitwise iterates as the C oracle, over V and W cycles, nu1 = 0,
+    coarsest_N 2 and 4, and the C1 / STAR5 / BOX9 / STAR7 smoother shapes (tests/env_path_case.py)."""
     import json
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.join(root, "tests"))
+    import env_path_case as epc
     r = subprocess.run([sys.executable, os.path.join(root, "tests", "env_path_case.py")], capture_output=True,
-                       text=True, timeout=600, env=dict(os.environ, **env))
+                       text=True, timeout=900, env=dict(os.environ, **env))
     assert r.returncode == 0, r.stderr[-3000:]
     got = json.loads(r.stdout.strip().splitlines()[-1])
-    for case, (cfg_id, sm, gamma, nu1, nu2, cN) in {"c1": ("c1", "m9", 1, 1, 1, 2), "c3": ("c3", "m7", 1, 1, 1, 2),
-                                                    "w64": ("c1", "m9", 2, 1, 0, 4)}.items():
-        b = workloads.rhs(cfg_id)
-        dim, N, _ = workloads.CONFIGS[cfg_id]
-        if case == "w64":
-            N, b = 64, np.random.default_rng(5).uniform(-1, 1, (63, 63))
+    for case, (src, sm, cyc, nu1, nu2, cN) in epc.CASES.items():
+        N, b = epc.case_rhs(src)
         M = sp.named(sm)
         uo, norms, k, conv = c_oracle.solve_history(b, N, npo.terms_of(M.stencil), M.omega_opt_analytic, nu1, nu2,
-                                                    gamma, cN)
+                                                    2 if cyc == "W" else 1, cN)
         it, hist, sha = got[case]
         assert it == k, (case, it, k)
         assert max(abs(a - r) / r for a, r in zip(hist, norms)) < 1e-8, case

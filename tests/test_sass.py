@@ -1,9 +1,10 @@
 """SASS guard of the bitwise contract: no fused multiply-add
 in any kernel that computes the iterate or the coarse right-hand side.  FMAs are allowed only
 where they are part of the contract or off the iterate path:
-  * the coarse LU solve (getrs order with FMA, Appendix A.6): k_coarse_solve, k_tail, k_cluster_tail;
+  * the coarse LU solve (getrs order with FMA, Appendix A.6, and the correctly rounded pivot
+    division): k_coarse_solve, k_tail;
   * the residual norm's sqrt (IEEE-rounded sqrt uses DFMA internally; the norm never feeds back):
-    the Mode 1/2 (norm) instantiations of the marching kernels, k_residual_norm, k_sweep_rr2d<..., true>.
+    the Mode 1/2 (norm) instantiations of the marching kernels, k_residual_norm.
 Runs on the CPU with cuobjdump on the in-tree library."""
 import os
 import re
@@ -34,13 +35,11 @@ def _fma_counts():
 
 
 def _allowed(name):
-    if any(k in name for k in ("k_coarse_solve", "k_tail<", "k_cluster_tail<", "k_residual_norm")):
+    if any(k in name for k in ("k_coarse_solve", "k_tail<", "k_residual_norm")):
         return True
     m = re.match(r"void spaimg::k_sweep(2d|3d)_march<\w+, \d+, (true|false), (\d)>", name)
     if m:
         return m.group(3) in ("1", "2")  # norm modes
-    if name.startswith("void spaimg::k_sweep_rr2d<"):
-        return name.split(">")[0].endswith("true")  # NORM
     return False
 
 
