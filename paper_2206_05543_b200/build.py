@@ -17,8 +17,8 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libspaimg_cuda.so")
 
-SOURCES = ["kernels_basic.cu", "kernels_sweep.cu", "kernels_sweep3d.cu", "kernels_restrict.cu", "kernels_tail.cu", "kernels_flat.cu", "kernels_rng.cu", "solver.cu"]
-HEADERS = ["spaimg_common.cuh", "kernels.h", "ptx.cuh", "march.cuh"]
+SOURCES = ["kernels_basic.cu", "kernels_sweep.cu", "kernels_sweep3d.cu", "kernels_restrict.cu", "kernels_tail.cu", "kernels_tail_fast2d.cu", "kernels_tail_fast3d.cu", "kernels_flat.cu", "kernels_rng.cu", "solver.cu"]
+HEADERS = ["spaimg_common.cuh", "kernels.h", "ptx.cuh", "march.cuh", "tail_ops.cuh", "kernels_tail_fast.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [

@@ -105,37 +105,44 @@ enum TailOpType : int {
     TAIL_FW = 4,       // coarse b = full weighting of r             (multigrid.py:104-119)
     TAIL_PROLONG = 5,  // x = x + P (coarse x)                       (multigrid.py:122-144, :184)
     TAIL_COARSE = 6,   // x = (LU)^-1 b in getrs order                (multigrid.py:147-154)
+    // fused ops of the compile-time engine (kernels_tail_fast.cuh; host-side labels only)
+    TAIL_RESFW = 7,        // RES + FW
+    TAIL_PROLONG_RES = 8,  // PROLONG + the next RES
 };
-// One op (host-recorded).  Array offsets are element offsets, from the start of the level-array
-// block, of each array's interior point 0:
-//   RES: a0 = x, a1 = b, a2 = r, s = sA     RELAX: a0 = x, a2 = r, s = sM
-//   RELAX0: a0 = x, a1 = b, s = sM           ZERO: a0 = x
-//   FW: a2 = fine r, a1 = coarse b           PROLONG: a0 = fine x, a1 = coarse x
-//   COARSE: a0 = x, a1 = b
-template <class T> struct alignas(16) TailOp {
-    int type;
-    int logw;       // the level's points are mapped onto a W^dim box, W = 1 << logw
-    int nw;         // warps executing the op (a prefix of the CTA)
-    int bw;         // warps meeting at the barrier before the op: max(nw of this op and the previous)
-    int bid;        // barrier for bw warps: 0 = __syncthreads, -1 = __syncwarp, else a named barrier id
-    int n;          // interior points per axis
-    int s0, s1;     // element pitch of axis 0 and (3D) axis 1
-    int a0, a1, a2;
-    int m, cs0, cs1;  // FW / PROLONG: the coarse level's interior size and pitches
+// One op = one packed word (host-recorded): type | level << 3 | nw << 6 | bw << 11 | bid << 16
+//   level: index into TailArgs::lv (0 = the entry level); FW / PROLONG also use level + 1
+//   nw:    warps executing the op (a prefix of the CTA)
+//   bw:    warps meeting at the barrier before the op: max(nw of this op and of the previous one)
+//   bid:   barrier for bw warps: 0 = __syncthreads, kTailSyncWarp = __syncwarp, else a named id
+constexpr int kTailMaxOps = 1536;
+constexpr int kTailMaxLevels = 8;
+constexpr int kTailMaxLU = 27;   // coarse systems up to 27 unknowns keep their factors in the parameters
+constexpr int kTailSyncWarp = 31;
+__host__ __device__ constexpr unsigned tail_op_word(int type, int level, int nw, int bw, int bid) {
+    return (unsigned)type | (unsigned)level << 3 | (unsigned)nw << 6 | (unsigned)bw << 11 | (unsigned)bid << 16;
+}
+// a level in the engine's shared memory: array offsets are element offsets, from the start of the
+// level-array block, of each array's interior point 0
+template <class T> struct TailLv {
+    int n;        // interior points per axis
+    int logw;     // the level's points are mapped onto a W^dim box, W = 1 << logw
+    int s0, s1;   // element pitch of axis 0 and (3D) axis 1
+    int x, b, r;  // arrays (r = -1 on the coarse level)
     int pad;
-    T s;
+    T sA, sM;
 };
+// Everything the engine reads per op lives in the kernel parameters (constant bank): the op
+// words, the level table and the coarse LU factors, so an op costs no shared-memory fetch and
+// the substitution's coefficients are DFMA constant operands.
 template <class T> struct TailArgs {
-    const TailOp<T>* ops;    // device array, nops entries
-    int nops;
-    const T* coarse;         // [nlu*nlu: -LU off the diagonal, row-major | U_jj (nlu) | 1/U_jj (nlu)]
-    const int* coarse_idx;   // [nlu: b offset of row perm[i] | nlu: x offset of unknown i]
-    int nlu;
-    int coarse_off;          // byte offset of the coarse data in shared memory
-    int arr_off;             // byte offset of the level-array block in shared memory
+    int nops, nlv, nlu;
+    int gamma, nu1, nu2;     // the cycle (the compile-time engine walks the recursion itself)
+    int entry_fz;            // the entry level starts from a zero iterate
+    int fast_le, fast_lc;    // > 0: the compile-time engine for entry / coarse levels of n = 2^le - 1 / 2^lc - 1
     int arr_elems;           // T elements of the level-array block
     int zero_from;           // elements [zero_from, arr_elems) are zeroed on entry (level 0's r onwards)
-    size_t smem;             // dynamic shared memory bytes
+    int frame;               // F: zero frame width of the shared-memory arrays (stencil radius)
+    size_t smem;             // dynamic shared memory bytes (the level arrays [+ the LU work vector])
     Terms<T> M;
     T omega;
     // the entry level: b and the start iterate come from its global buffers (zero frames
@@ -143,11 +150,28 @@ template <class T> struct TailArgs {
     Layout gL;
     const T* gb;
     T* gx;
-    int frame;               // F: zero frame width of the shared-memory arrays (stencil radius)
-    int e_s0, e_s1;          // shared-memory pitches of the entry level
-    int e_x, e_b;            // interior offsets of the entry level's x and b
     int shape;               // SHAPE_* of M: named shapes get compile-time stencil offsets
+    long long* prof;         // diagnostics (SPAIMG_TAIL_PROF=1): clock64() at the start of each op
+    // coarse factors for nlu > kTailMaxLU (global memory; copied to shared memory on entry)
+    const T* coarse_g;       // [nlu*nlu: -LU off the diagonal, row-major | U_jj | 1/U_jj]
+    const int* coarse_idx_g; // [b offsets of the permuted rows | x offsets]
+    TailLv<T> lv[kTailMaxLevels];
+    // coarse factors for nlu <= kTailMaxLU: row-major -LU off the diagonal, U_jj, 1/U_jj, and the
+    // b offsets of the permuted rows / x offsets of the unknowns (getrs row interchanges folded in)
+    T lu[kTailMaxLU * kTailMaxLU];
+    T dg[kTailMaxLU], rc[kTailMaxLU];
+    int cin[kTailMaxLU], cout[kTailMaxLU];
+    unsigned ops[kTailMaxOps];
 };
 template <class T> cudaError_t launch_tail(const TailArgs<T>& a, cudaStream_t s);
+// the compile-time engine (kernels_tail_fast{2,3}d.cu): which entry / coarse sizes and shapes it
+// is instantiated for; cudaErrorNotSupported otherwise
+constexpr int kTailFastLE2 = 6, kTailFastLE3 = 4;
+inline bool tail_fast_shape(int dim, int shape) {
+    return dim == 2 ? (shape == SHAPE_C1 || shape == SHAPE_STAR5 || shape == SHAPE_BOX9)
+                    : (shape == SHAPE_C1 || shape == SHAPE_STAR7);
+}
+template <class T> cudaError_t launch_tail_fast2d(const TailArgs<T>& a, cudaStream_t s);
+template <class T> cudaError_t launch_tail_fast3d(const TailArgs<T>& a, cudaStream_t s);
 
 }  // namespace spaimg

@@ -437,11 +437,9 @@ template <class T> struct Solver final : spaimg_solver {
     std::vector<std::pair<long long, cudaGraphExec_t>> op_graphs;
     // shared-memory coarse engine (K5+): levels >= tail_l (if < nsmooth()) run in one CTA per visit
     int tail_l = 1 << 30;
-    TailOp<T>* tail_ops[2] = {};  // uploaded op lists for an entry from a given iterate / from zero
-    int tail_nops[2] = {};
-    T* tail_coarse = nullptr;     // coarse LU data in the engine's format
+    TailArgs<T> tail_args[2] = {};  // complete launch parameters for an entry from a given iterate / from zero
+    T* tail_coarse = nullptr;       // coarse factors for nlu > kTailMaxLU
     int* tail_coarse_idx = nullptr;
-    TailArgs<T> tail_args{};      // everything but the op list and the entry buffers
 
     ~Solver() override {
         if (bs_h2d) {
@@ -584,11 +582,10 @@ template <class T> struct Solver final : spaimg_solver {
     }
 
     // ---- shared-memory engine plan ------------------------------------------------------
-    struct TGeo {
-        int n, logw, w, s0, s1, x, b, r;
-        T sA, sM;
+    struct HOp {
+        int type, level, nw, bw, bid;
     };
-    std::vector<TGeo> tg;  // tail levels: tg[0] = entry level ... tg.back() = coarse level
+    std::vector<TailLv<T>> tg;  // tail levels: tg[0] = entry level ... tg.back() = coarse level
 
     static int ceil_log2(int n) {
         int k = 0;
@@ -606,13 +603,13 @@ template <class T> struct Solver final : spaimg_solver {
         tg.clear();
         int cur = 0;
         for (int l = l0; l <= nsmooth(); ++l) {
-            TGeo g{};
+            TailLv<T> g{};
             g.n = lv[l].L.n;
             g.logw = ceil_log2(g.n);
-            g.w = g.n + 2 * F;
-            g.s0 = cfg.dim == 2 ? g.w : g.w * g.w;
-            g.s1 = cfg.dim == 3 ? g.w : 0;
-            const int size = (cfg.dim == 2 ? g.w * g.w : g.w * g.w * g.w + 1) / 2 * 2;  // 16-byte multiples
+            const int w = g.n + 2 * F;
+            g.s0 = cfg.dim == 2 ? w : w * w;
+            g.s1 = cfg.dim == 3 ? w : 0;
+            const int size = ((cfg.dim == 2 ? w * w : w * w * w) + 1) / 2 * 2;  // 16-byte multiples
             const int origin = F * g.s0 + F * g.s1 + F;
             g.x = cur + origin;
             cur += size;
@@ -633,41 +630,16 @@ template <class T> struct Solver final : spaimg_solver {
         return cur + 2 * tg[0].s0 + 2 * tg[0].s1 + 2;
     }
 
-    TailOp<T> point_op(int type, int i) const {
-        const TGeo& g = tg[i];
-        TailOp<T> o{};
-        o.type = type;
-        o.logw = g.logw;
-        o.nw = warps_for(cfg.dim, g.logw);
-        o.n = g.n;
-        o.s0 = g.s0;
-        o.s1 = g.s1;
-        o.a0 = g.x;
-        o.a1 = g.b;
-        o.a2 = g.r;
-        o.s = type == TAIL_RES ? g.sA : g.sM;
-        if (type == TAIL_FW || type == TAIL_PROLONG) {
-            const TGeo& c = tg[i + 1];
-            o.nw = type == TAIL_FW ? warps_for(cfg.dim, g.logw - 1) : o.nw;
-            o.a1 = type == TAIL_FW ? c.b : c.x;
-            o.m = c.n;
-            o.cs0 = c.s0;
-            o.cs1 = c.s1;
-        }
-        return o;
+    HOp point_op(int type, int i) const {
+        const int logw = type == TAIL_FW ? tg[i].logw - 1 : tg[i].logw;
+        return HOp{type, i, warps_for(cfg.dim, logw), 0, 0};
     }
 
     // the recursion of visit() (multigrid.py:157-185) below the entry level, as engine ops
-    void record(int i, bool fz, std::vector<TailOp<T>>& ops) const {
+    void record(int i, bool fz, std::vector<HOp>& ops) const {
         const int last = (int)tg.size() - 1;
         if (i == last) {  // u.N <= coarsest_N: direct solve (multigrid.py:166-167)
-            TailOp<T> o{};
-            o.type = TAIL_COARSE;
-            o.nw = (nlu == 1 || nlu == 9 || nlu == 27 || nlu <= 32) ? 1 : kTailThreads / 32;
-            o.n = tg[i].n;
-            o.a0 = tg[i].x;
-            o.a1 = tg[i].b;
-            ops.push_back(o);
+            ops.push_back(HOp{TAIL_COARSE, i, nlu <= kTailMaxLU ? 1 : kTailThreads / 32, 0, 0});
             return;
         }
         for (int k = 0; k < cfg.nu1; ++k) {
@@ -682,7 +654,10 @@ template <class T> struct Solver final : spaimg_solver {
         ops.push_back(point_op(TAIL_RES, i));
         ops.push_back(point_op(TAIL_FW, i));
         record(i + 1, true, ops);
-        for (int g = 1; g < cfg.gamma; ++g) record(i + 1, false, ops);
+        // the restricted system of the coarsest level is solved once, whatever gamma
+        // (multigrid.py:178-179)
+        if (i + 1 < last)
+            for (int g = 1; g < cfg.gamma; ++g) record(i + 1, false, ops);
         ops.push_back(point_op(TAIL_PROLONG, i));
         for (int k = 0; k < cfg.nu2; ++k) {
             ops.push_back(point_op(TAIL_RES, i));
@@ -690,20 +665,68 @@ template <class T> struct Solver final : spaimg_solver {
         }
     }
 
+    // the op sequence of the compile-time engine (kernels_tail_fast.cuh visit()), for the
+    // SPAIMG_TAIL_PROF labels
+    // kernels_tail_fast.cuh FastTail::NTH / fuse_rr / fuse_pr
+    int fast_nth(int) const { return kTailThreads; }
+    bool fast_fuse_rr(int i) const {
+        const int lw = tg[i].logw;
+        if (i + 1 >= (int)tg.size()) return false;
+        return (1LL << (cfg.dim * (lw - 1))) <= fast_nth(i + 1) && (cfg.dim == 2 || lw <= 3);
+    }
+    bool fast_fuse_pr(int i) const {
+        return i + 1 < (int)tg.size() && (1LL << (cfg.dim * tg[i].logw)) <= fast_nth(i);
+    }
+    void record_fast(int i, bool fz, bool res_done, bool res_next, std::vector<HOp>& ops) const {
+        const int last = (int)tg.size() - 1;
+        for (int k = 0; k < cfg.nu1; ++k) {
+            if (fz && k == 0) {
+                ops.push_back(point_op(TAIL_RELAX0, i));
+            } else if (res_done && k == 0) {
+                ops.push_back(point_op(TAIL_RELAX, i));
+            } else {
+                ops.push_back(point_op(TAIL_RES, i));
+                ops.push_back(point_op(TAIL_RELAX, i));
+            }
+        }
+        if (fz && cfg.nu1 == 0) ops.push_back(point_op(TAIL_ZERO, i));
+        if (fast_fuse_rr(i)) {
+            HOp o = point_op(TAIL_FW, i);
+            o.type = TAIL_RESFW;
+            ops.push_back(o);
+        } else {
+            ops.push_back(point_op(TAIL_RES, i));
+            ops.push_back(point_op(TAIL_FW, i));
+        }
+        if (i + 1 == last) {
+            ops.push_back(HOp{TAIL_COARSE, last, 1, 0, 0});
+        } else {
+            const bool sib = fast_fuse_pr(i + 1) && cfg.nu1 >= 1 && cfg.nu2 == 0;
+            for (int g = 0; g < cfg.gamma; ++g) record_fast(i + 1, g == 0, sib && g > 0, sib && g + 1 < cfg.gamma, ops);
+        }
+        HOp o = point_op(TAIL_PROLONG, i);
+        if (fast_fuse_pr(i) && (cfg.nu2 >= 1 || res_next)) o.type = TAIL_PROLONG_RES;
+        ops.push_back(o);
+        for (int k = 0; k < cfg.nu2; ++k) {
+            if (!(k == 0 && fast_fuse_pr(i))) ops.push_back(point_op(TAIL_RES, i));
+            ops.push_back(point_op(TAIL_RELAX, i));
+        }
+    }
+
     // barrier plan: op i waits with the warps of ops i-1 and i (always a prefix of the CTA); one
     // named barrier id per distinct warp count -- warps that skip small ops run ahead and must
     // not share a barrier with a different count
-    int tail_barriers(std::vector<TailOp<T>>& ops) const {
+    int tail_barriers(std::vector<HOp>& ops) const {
         std::vector<int> counts;
         const int all = kTailThreads / 32;
         int prev = all;
-        for (TailOp<T>& o : ops) {
+        for (HOp& o : ops) {
             o.bw = std::max(o.nw, prev);
             prev = o.nw;
             if (o.bw == all) {
                 o.bid = 0;
             } else if (o.bw == 1) {
-                o.bid = -1;
+                o.bid = kTailSyncWarp;
             } else {
                 auto it = std::find(counts.begin(), counts.end(), o.bw);
                 if (it == counts.end()) {
@@ -729,34 +752,29 @@ template <class T> struct Solver final : spaimg_solver {
         int l0 = nsmooth();
         while (l0 > 1 && lv[l0 - 1].L.N <= thr && lv[l0 - 1].L.n <= nmax) --l0;  // the finest level never joins
         if (l0 >= nsmooth()) return 0;
-        // shrink the engine until its levels fit in one CTA's shared memory
-        std::vector<TailOp<T>> ops[2];
-        int arr_elems = 0, zero_from = 0, coarse_off = 0, arr_off = 0;
+        // shrink the engine until its levels fit in one CTA's shared memory and its op lists in
+        // the launch parameters
+        std::vector<HOp> ops[2];
+        int arr_elems = 0, zero_from = 0;
         size_t smem = 0;
-        const size_t ncf = (size_t)nlu * nlu + 2 * (size_t)nlu;
         for (; l0 < nsmooth(); ++l0) {
+            if (nsmooth() + 1 - l0 > kTailMaxLevels) continue;
             arr_elems = plan_geometry(l0, F, &zero_from);
             for (int fz = 0; fz < 2; ++fz) {
                 ops[fz].clear();
                 record(0, fz != 0, ops[fz]);
                 if (int rc = tail_barriers(ops[fz])) return rc;
             }
-            const size_t nops = std::max(ops[0].size(), ops[1].size());
-            coarse_off = (int)(nops * sizeof(TailOp<T>));
-            arr_off = (int)((coarse_off + ncf * sizeof(T) + 2 * (size_t)nlu * sizeof(int) + 15) / 16 * 16);
-            smem = arr_off + ((size_t)arr_elems + (nlu > 32 ? nlu : 0)) * sizeof(T);
+            if ((int)std::max(ops[0].size(), ops[1].size()) > kTailMaxOps) continue;
+            smem = ((size_t)arr_elems + (nlu > kTailMaxLU ? (size_t)nlu * nlu + 3 * (size_t)nlu + 2 : 0)) * sizeof(T) +
+                   (nlu > kTailMaxLU ? (2 * (size_t)nlu + 2) * sizeof(int) : 0);
             if (smem <= (size_t)optin) break;
         }
         if (l0 >= nsmooth()) return 0;
         tail_l = l0;
-        for (int fz = 0; fz < 2; ++fz) {
-            if (int rc = dalloc(&tail_ops[fz], ops[fz].size())) return rc;
-            CK(cudaMemcpy(tail_ops[fz], ops[fz].data(), ops[fz].size() * sizeof(TailOp<T>), cudaMemcpyHostToDevice));
-            tail_nops[fz] = (int)ops[fz].size();
-        }
         // coarse data: -LU off the diagonal, U_jj, 1/U_jj (correctly rounded host division);
         // the row interchanges of getrs (laswp) folded into a gather order
-        std::vector<T> cf(ncf);
+        std::vector<T> cf((size_t)nlu * nlu + 2 * (size_t)nlu);
         for (int i = 0; i < nlu; ++i)
             for (int j = 0; j < nlu; ++j) cf[(size_t)i * nlu + j] = i == j ? T(0) : (T)(-lu_h[(size_t)i * nlu + j]);
         for (int j = 0; j < nlu; ++j) {
@@ -767,7 +785,7 @@ template <class T> struct Solver final : spaimg_solver {
         std::vector<int> perm(nlu), ci(2 * (size_t)nlu);
         for (int i = 0; i < nlu; ++i) perm[i] = i;
         for (int i = 0; i < nlu; ++i) std::swap(perm[i], perm[piv_h[i]]);
-        const TGeo& cg = tg.back();
+        const TailLv<T>& cg = tg.back();
         auto off = [&](int q) {
             const int n = cg.n;
             if (cfg.dim == 2) return (q / n) * cg.s0 + q % n;
@@ -777,40 +795,108 @@ template <class T> struct Solver final : spaimg_solver {
             ci[i] = off(perm[i]);
             ci[nlu + i] = off(i);
         }
-        if (int rc = dalloc(&tail_coarse, ncf)) return rc;
-        CK(cudaMemcpy(tail_coarse, cf.data(), ncf * sizeof(T), cudaMemcpyHostToDevice));
-        if (int rc = dalloc(&tail_coarse_idx, ci.size())) return rc;
-        CK(cudaMemcpy(tail_coarse_idx, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
-        TailArgs<T>& ta = tail_args;
-        ta.coarse = tail_coarse;
-        ta.coarse_idx = tail_coarse_idx;
-        ta.nlu = nlu;
-        ta.coarse_off = coarse_off;
-        ta.arr_off = arr_off;
-        ta.arr_elems = arr_elems;
-        ta.zero_from = zero_from;
-        ta.smem = smem;
-        ta.M = M;
-        ta.omega = omega;
-        ta.gL = lv[l0].L;
-        ta.frame = F;
-        ta.e_s0 = tg[0].s0;
-        ta.e_s1 = tg[0].s1;
-        ta.e_x = tg[0].x;
-        ta.e_b = tg[0].b;
-        ta.shape = shape;
+        if (nlu > kTailMaxLU) {
+            if (int rc = dalloc(&tail_coarse, cf.size())) return rc;
+            CK(cudaMemcpy(tail_coarse, cf.data(), cf.size() * sizeof(T), cudaMemcpyHostToDevice));
+            if (int rc = dalloc(&tail_coarse_idx, ci.size())) return rc;
+            CK(cudaMemcpy(tail_coarse_idx, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
+        }
+        long long* prof = nullptr;
+        const char* ep = getenv("SPAIMG_TAIL_PROF");
+        if (ep && ep[0] == '1')
+            if (int rc = dalloc(&prof, (size_t)3 * kTailMaxOps + 1)) return rc;
+        // the compile-time engine: a power-of-two hierarchy from the instantiated entry size down to
+        // a coarse level of 1 or 3 points per axis, frame 1, a named smoother shape
+        const int le = cfg.dim == 2 ? kTailFastLE2 : kTailFastLE3;
+        bool fast = F == 1 && tail_fast_shape(cfg.dim, shape) && tg[0].n == (1 << le) - 1;
+        for (size_t i = 0; i < tg.size(); ++i) fast = fast && tg[i].n == (1 << (le - (int)i)) - 1;
+        const int lc = le - (int)tg.size() + 1;
+        fast = fast && (lc == 1 || lc == 2);
+        const char* ef = getenv("SPAIMG_TAIL_FAST");
+        if (ef && ef[0] == '0') fast = false;
+        for (int fz = 0; fz < 2; ++fz) {
+            TailArgs<T>& ta = tail_args[fz];
+            ta.gamma = cfg.gamma;
+            ta.nu1 = cfg.nu1;
+            ta.nu2 = cfg.nu2;
+            ta.entry_fz = fz;
+            ta.fast_le = fast ? le : 0;
+            ta.fast_lc = fast ? lc : 0;
+            ta.nops = (int)ops[fz].size();
+            ta.nlv = (int)tg.size();
+            ta.nlu = nlu;
+            ta.arr_elems = arr_elems;
+            ta.zero_from = zero_from;
+            ta.frame = F;
+            ta.smem = smem;
+            ta.M = M;
+            ta.omega = omega;
+            ta.gL = lv[l0].L;
+            ta.shape = shape;
+            ta.prof = prof;
+            ta.coarse_g = tail_coarse;
+            ta.coarse_idx_g = tail_coarse_idx;
+            for (size_t i = 0; i < tg.size(); ++i) ta.lv[i] = tg[i];
+            if (nlu <= kTailMaxLU) {
+                for (int i = 0; i < nlu; ++i)
+                    for (int j = 0; j < nlu; ++j) ta.lu[i * nlu + j] = cf[(size_t)i * nlu + j];
+                for (int j = 0; j < nlu; ++j) {
+                    ta.dg[j] = cf[(size_t)nlu * nlu + j];
+                    ta.rc[j] = cf[(size_t)nlu * nlu + nlu + j];
+                    ta.cin[j] = ci[j];
+                    ta.cout[j] = ci[nlu + j];
+                }
+            }
+            for (size_t i = 0; i < ops[fz].size(); ++i) {
+                const HOp& o = ops[fz][i];
+                ta.ops[i] = tail_op_word(o.type, o.level, o.nw, o.bw, o.bid);
+            }
+        }
+        prof_ops[0] = ops[0];
+        prof_ops[1] = ops[1];
+        if (fast)
+            for (int fz = 0; fz < 2; ++fz) {
+                prof_ops[fz].clear();
+                record_fast(0, fz != 0, false, false, prof_ops[fz]);
+            }
         return 0;
+    }
+
+    // diagnostics: per-op cycles of the last engine launch (SPAIMG_TAIL_PROF=1, eager runs)
+    std::vector<HOp> prof_ops[2];
+    int prof_last_fz = 0;
+    void tail_profile_dump() {
+        if (!tail_args[0].prof) return;
+        const std::vector<HOp>& ops = prof_ops[prof_last_fz];
+        std::vector<long long> c(3 * kTailMaxOps + 1);
+        if (cudaDeviceSynchronize() != cudaSuccess) return;
+        cudaMemcpy(c.data(), tail_args[0].prof, c.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+        c[ops.size()] = c[ops.size()];
+        static const char* names[] = {"RES", "RELAX", "RELAX0", "ZERO", "FW", "PROLONG", "COARSE", "RESFW", "PRORES"};
+        long long tot[9] = {}, cnt[9] = {};
+        for (size_t i = 0; i < ops.size(); ++i) {
+            const long long d = c[i + 1] - c[i];
+            tot[ops[i].type] += d;
+            cnt[ops[i].type] += 1;
+            const bool split = ops[i].type != TAIL_COARSE && !tail_args[0].fast_le;
+            const long long pre = split ? c[kTailMaxOps + i] - c[i] : 0;
+            const long long body = split ? c[2 * kTailMaxOps + i] - c[kTailMaxOps + i] : 0;
+            fprintf(stderr, "tailprof op %3zu %-7s n=%2d nw=%2d bw=%2d  %6lld cycles (dispatch %lld body %lld)\n", i,
+                    names[ops[i].type], tg[ops[i].level].n, ops[i].nw, ops[i].bw, d, pre, body);
+        }
+        for (int k = 0; k < 9; ++k)
+            if (cnt[k]) fprintf(stderr, "tailprof sum %-7s %3lld ops %8lld cycles\n", names[k], cnt[k], tot[k]);
+        fprintf(stderr, "tailprof total %lld cycles\n", c[ops.size()] - c[0]);
     }
 
     // one visit of the engine's entry level: x[a] updated in place
     int tail_visit(int l, int a, bool fz, cudaStream_t s, int* launches) {
         if (l != tail_l) return -1;
-        TailArgs<T> ta = tail_args;
         const int z = fz ? 1 : 0;
-        ta.ops = tail_ops[z];
-        ta.nops = tail_nops[z];
+        TailArgs<T>& ta = tail_args[z];
         ta.gb = lv[l].b;
         ta.gx = lv[l].x[a];
+        prof_last_fz = z;
         if (launch_tail<T>(ta, s) != cudaSuccess) return -1;
         ++*launches;
         return a;
@@ -1035,6 +1121,7 @@ template <class T> struct Solver final : spaimg_solver {
                 if (int rc = norm_launch(lv[0].x[0], s, &launches)) return rc;
             }
         }
+        tail_profile_dump();
         return 0;
     }
 

@@ -258,7 +258,7 @@ def test_solve_batch_pipelined_matches_single_solves(dim, N, sm):
         assert np.array_equal(u.numpy(), ref_u.values)
 
 
-@pytest.mark.parametrize("env", [{}, {"SPAIMG_NO_GRAPH": "1"}, {"SPAIMG_TAIL_N": "0"}, {"SPAIMG_TAIL_N": "8"},
+@pytest.mark.parametrize("env", [{}, {"SPAIMG_NO_GRAPH": "1"}, {"SPAIMG_TAIL_FAST": "0"}, {"SPAIMG_TAIL_N": "0"}, {"SPAIMG_TAIL_N": "8"},
                                  {"SPAIMG_TAIL_N": "32"}, {"SPAIMG_FLAT_N2": "0", "SPAIMG_FLAT_N3": "0"}],
                          ids=lambda e: ",".join(f"{k[7:]}={v}" for k, v in e.items()) or "default")
 def test_alternate_paths_bitwise(env):
