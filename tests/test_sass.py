@@ -2,7 +2,7 @@
 in any kernel that computes the iterate or the coarse right-hand side.  FMAs are allowed only
 where they are part of the contract or off the iterate path:
   * the coarse LU solve (getrs order with FMA, Appendix A.6, and the correctly rounded pivot
-    division): k_coarse_solve, k_tail;
+    division): k_coarse_solve, k_tail, k_tail_fast;
   * the residual norm's sqrt (IEEE-rounded sqrt uses DFMA internally; the norm never feeds back):
     the Mode 1/2 (norm) instantiations of the marching kernels, k_residual_norm.
 Runs on the CPU with cuobjdump on the in-tree library."""
@@ -35,7 +35,7 @@ def _fma_counts():
 
 
 def _allowed(name):
-    if any(k in name for k in ("k_coarse_solve", "k_tail<", "k_residual_norm")):
+    if any(k in name for k in ("k_coarse_solve", "k_tail<", "k_tail_fast<", "k_residual_norm")):
         return True
     m = re.match(r"void spaimg::k_sweep(2d|3d)_march<\w+, \d+, (true|false), (\d)>", name)
     if m:
