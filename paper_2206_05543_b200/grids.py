@@ -16,11 +16,12 @@ __all__ = ["Grid", "is_device_array"]
 
 
 def is_device_array(v) -> bool:
+    """True for CUDA tensors only; CPU torch tensors count as host arrays."""
     try:
         import torch
     except ImportError:  # pragma: no cover
         return False
-    return isinstance(v, torch.Tensor)
+    return isinstance(v, torch.Tensor) and v.is_cuda
 
 
 @dataclass

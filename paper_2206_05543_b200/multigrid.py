@@ -10,10 +10,14 @@ Extensions over the reference (all optional, defaults reproduce it):
   * `solve(b, cfg, u0=None)`: u0=None draws the reference's seeded U(0,1) start
     (multigrid.py:204-205) on the host; pass an array/Grid (or 0) to start elsewhere.
   * float32 device grids (torch float32 tensors) run the fp32 kernels.
+  * `solve`/`cycle` keep their device hierarchy and captured graphs between calls
+    (`cached_solver`, the counterpart of the reference's lru_cache on the coarse LU).
 """
 
 import ctypes
+import threading
 import time
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -31,6 +35,8 @@ __all__ = [
     "cycle",
     "solve",
     "Solver",
+    "cached_solver",
+    "clear_solver_cache",
 ]
 
 
@@ -118,16 +124,47 @@ def _stencil_struct(S) -> _lib.SpaimgStencil:
 
 
 class _Arr:
-    """A grid's values as a raw pointer for the C ABI (keeps the owner alive)."""
+    """A grid's values as a raw pointer for the C ABI (keeps the owner alive).
 
-    def __init__(self, values, dtype_code):
-        self.owner = values
+    Device inputs/outputs must be contiguous CUDA tensors of the call's dtype and shape.  Host
+    inputs are converted (copied) as needed; host OUTPUTS must already be C-contiguous, writeable
+    numpy arrays of the right dtype and shape, since a converted copy would leave the caller's
+    array unchanged.
+    """
+
+    def __init__(self, values, dtype_code, shape=None, out=False, device=None):
+        npdt = np.float64 if dtype_code == _lib.F64 else np.float32
         if is_device_array(values):
+            import torch
+            want = torch.float64 if dtype_code == _lib.F64 else torch.float32
+            if values.dtype != want:
+                raise TypeError(f"device array has dtype {values.dtype}, expected {want}")
+            if not values.is_contiguous():
+                raise ValueError("device array must be contiguous")
+            if device is not None and values.device.index != device:
+                raise ValueError(f"device array on cuda:{values.device.index}, expected cuda:{device}")
+            if shape is not None and tuple(values.shape) != tuple(shape):
+                raise ValueError(f"array shape {tuple(values.shape)} does not match {tuple(shape)}")
+            self.owner = values
             self.ptr = values.data_ptr()
+            return
+        try:
+            import torch
+            if isinstance(values, torch.Tensor):  # CPU tensor: a host array
+                values = values.detach().numpy()
+        except ImportError:  # pragma: no cover
+            pass
+        if out:
+            if not (isinstance(values, np.ndarray) and values.dtype == npdt and values.flags.c_contiguous
+                    and values.flags.writeable):
+                raise TypeError(f"host output must be a writeable C-contiguous {np.dtype(npdt).name} numpy array")
+            a = values
         else:
-            a = np.ascontiguousarray(values, dtype=np.float64 if dtype_code == _lib.F64 else np.float32)
-            self.owner = a
-            self.ptr = a.ctypes.data
+            a = np.ascontiguousarray(values, dtype=npdt)
+        if shape is not None and tuple(a.shape) != tuple(shape):
+            raise ValueError(f"array shape {tuple(a.shape)} does not match {tuple(shape)}")
+        self.owner = a
+        self.ptr = a.ctypes.data
 
 
 def _dtype_code(values) -> int:
@@ -178,7 +215,7 @@ def apply_stencil(S, u: Grid) -> Grid:
     stream = _stream_for(u.values)
     x = _Arr(u.values, code)
     out = _empty_like(u.values, tuple(u.values.shape))
-    o = _Arr(out, code)
+    o = _Arr(out, code, out=True)
     st = _stencil_struct(S)
     _lib.check(lib.spaimg_apply(code, u.N, ctypes.byref(st), x.ptr, o.ptr, stream))
     return Grid(u.N, out)
@@ -198,7 +235,7 @@ def smooth(u: Grid, b: Grid, M, omega: float, steps: int) -> Grid:
     x = _Arr(u.values, code)
     bb = _Arr(_same_side(u.values, b.values), code)
     out = _empty_like(u.values, tuple(u.values.shape))
-    o = _Arr(out, code)
+    o = _Arr(out, code, out=True)
     st = _stencil_struct(M)
     _lib.check(lib.spaimg_smooth(code, u.dim, u.N, x.ptr, bb.ptr, ctypes.byref(st), float(omega), int(steps),
                                  o.ptr, stream))
@@ -217,7 +254,7 @@ def restrict(fine: Grid) -> Grid:
     x = _Arr(fine.values, code)
     Nc = fine.N // 2
     out = _empty_like(fine.values, (Nc - 1,) * fine.dim)
-    o = _Arr(out, code)
+    o = _Arr(out, code, out=True)
     _lib.check(lib.spaimg_restrict(code, fine.dim, fine.N, x.ptr, o.ptr, stream))
     return Grid(Nc, out)
 
@@ -231,7 +268,7 @@ def prolong(coarse: Grid, fine_N: int) -> Grid:
     stream = _stream_for(coarse.values)
     e = _Arr(coarse.values, code)
     out = _empty_like(coarse.values, (fine_N - 1,) * coarse.dim)
-    o = _Arr(out, code)
+    o = _Arr(out, code, out=True)
     _lib.check(lib.spaimg_prolong(code, coarse.dim, coarse.N, e.ptr, o.ptr, stream))
     return Grid(fine_N, out)
 
@@ -251,7 +288,7 @@ def residual_restrict(u: Grid, b: Grid) -> Grid:
     bb = _Arr(_same_side(u.values, b.values), code)
     Nc = u.N // 2
     out = _empty_like(u.values, (Nc - 1,) * u.dim)
-    o = _Arr(out, code)
+    o = _Arr(out, code, out=True)
     _lib.check(lib.spaimg_residual_restrict(code, u.dim, u.N, x.ptr, bb.ptr, o.ptr, stream))
     return Grid(Nc, out)
 
@@ -266,7 +303,7 @@ def prolong_correct(u: Grid, e: Grid) -> Grid:
     x = _Arr(u.values, code)
     ee = _Arr(_same_side(u.values, e.values), code)
     out = _empty_like(u.values, tuple(u.values.shape))
-    o = _Arr(out, code)
+    o = _Arr(out, code, out=True)
     _lib.check(lib.spaimg_prolong_correct(code, u.dim, u.N, x.ptr, ee.ptr, o.ptr, stream))
     return Grid(u.N, out)
 
@@ -316,9 +353,14 @@ def _coarse_level(N: int, coarsest_N: int) -> int:
 
 
 def _mg_struct(cfg: MgConfig, dim: int, N: int, dtype_code: int):
-    M, omega = cfg.resolve_smoother()
-    if M.dim != dim:
-        raise ValueError(f"smoother dim {M.dim} != grid dim {dim}")
+    if N <= cfg.coarsest_N:
+        # u.N <= coarsest_N: the cycle is the direct solve alone and the reference never looks at
+        # the smoother (multigrid.py:166-167); any radius-1 stencil fills the unused slot
+        M, omega = laplacian(dim), 0.0
+    else:
+        M, omega = cfg.resolve_smoother()
+        if M.dim != dim:
+            raise ValueError(f"smoother dim {M.dim} != grid dim {dim}")
     Nc = _coarse_level(N, cfg.coarsest_N)
     lu, piv = _coarsest_lu(dim, Nc)
     c = _lib.SpaimgMgConfig()
@@ -338,21 +380,67 @@ def _mg_struct(cfg: MgConfig, dim: int, N: int, dtype_code: int):
     return c, (lu, piv)
 
 
+# ------------------------------------------------------------------------------------------
+# cached solver handles: the reference's only expensive setup is the coarse LU, which it caches
+# (lru_cache, multigrid.py:147-149); here the setup is the device hierarchy and the captured
+# graphs, cached the same way per (device, dtype, dim, N, smoother terms, omega, cycle shape)
+# ------------------------------------------------------------------------------------------
+_SOLVER_CACHE = OrderedDict()
+_SOLVER_CACHE_MAX = 4
+_SOLVER_LOCK = threading.Lock()
+
+
+def _solver_key(cfg: MgConfig, dim: int, N: int, dtype_code: int, device: int):
+    if N <= cfg.coarsest_N:
+        sm = None
+    else:
+        M, omega = cfg.resolve_smoother()
+        sm = (int(M.dim), int(M.h_exponent), tuple((tuple(int(v) for v in o), float(c)) for o, c in M.entries.items()),
+              float(omega))
+    return (device, dtype_code, dim, N, sm, 2 if cfg.cycle == "W" else 1, int(cfg.nu1), int(cfg.nu2),
+            int(cfg.coarsest_N))
+
+
+def cached_solver(cfg: MgConfig, dim: int, N: int, dtype_code: int, device: int = 0) -> "Solver":
+    """The Solver for this problem shape, created on first use and kept (LRU, 4 entries); the
+    cache holds device memory, clear_solver_cache() releases it."""
+    key = _solver_key(cfg, dim, N, dtype_code, device)
+    with _SOLVER_LOCK:
+        s = _SOLVER_CACHE.get(key)
+        if s is not None:
+            _SOLVER_CACHE.move_to_end(key)
+            return s
+    s = Solver(cfg, dim, N, dtype="float32" if dtype_code == _lib.F32 else "float64", device=device)
+    with _SOLVER_LOCK:
+        _SOLVER_CACHE[key] = s
+        while len(_SOLVER_CACHE) > _SOLVER_CACHE_MAX:
+            _SOLVER_CACHE.popitem(last=False)
+    return s
+
+
+def clear_solver_cache():
+    with _SOLVER_LOCK:
+        _SOLVER_CACHE.clear()
+
+
+def _device_of(values) -> int:
+    return (values.device.index or 0) if is_device_array(values) else 0
+
+
 def cycle(u: Grid, b: Grid, cfg: MgConfig) -> Grid:
     """One multigrid cycle for A*u = b at the grid's resolution (multigrid.py:157-185)."""
     if u.N != b.N or u.dim != b.dim:
         raise ValueError("u and b must live on the same grid")
-    lib = _lib.load()
+    _lib.load()
     code = _dtype_code(u.values)
-    if u.N > cfg.coarsest_N:
-        cfg.resolve_smoother()  # reference raises here before anything else (multigrid.py:169)
-    c, keep = _mg_struct(cfg, u.dim, u.N, code)
+    dev = _device_of(u.values)
     stream = _stream_for(u.values)
-    x = _Arr(u.values, code)
-    bb = _Arr(_same_side(u.values, b.values), code)
+    s = cached_solver(cfg, u.dim, u.N, code, dev)
     out = _empty_like(u.values, tuple(u.values.shape))
-    o = _Arr(out, code)
-    _lib.check(lib.spaimg_cycle(ctypes.byref(c), x.ptr, bb.ptr, o.ptr, stream))
+    with s.lock:
+        s.load(_same_side(u.values, b.values), u.values, stream=stream.value)
+        s.cycles(1, stream=stream.value)
+        s.store(out, stream=stream.value)
     return Grid(u.N, out)
 
 
@@ -398,34 +486,30 @@ def _start_values(b: Grid, cfg: MgConfig, u0):
 def solve(b: Grid, cfg: MgConfig, u0=None) -> tuple:
     """Run cycles from the start until ||r_k|| <= tol ||r_0|| or max_iters (multigrid.py:188-227).
 
-    Returns (solution Grid, SolveReport); rho_hat = (||r_K|| / ||r_0||)**(1/K).
+    Returns (solution Grid, SolveReport); rho_hat = (||r_K|| / ||r_0||)**(1/K).  The device
+    hierarchy and graphs are cached across calls (cached_solver).
     """
     _check_solve(b, cfg)
-    lib = _lib.load()
+    _lib.load()
     code = _dtype_code(b.values)
-    c, keep = _mg_struct(cfg, b.dim, b.N, code)
+    dev = _device_of(b.values)
     stream = _stream_for(b.values)
     t0 = time.perf_counter()
+    s = cached_solver(cfg, b.dim, b.N, code, dev)
     start = _start_values(b, cfg, u0)
-    bb = _Arr(b.values, code)
-    uu = _Arr(start, code) if start is not None else None
     out = _empty_like(b.values, tuple(b.values.shape))
-    o = _Arr(out, code)
-    norms = (ctypes.c_double * (cfg.max_iters + 1))()
-    iters = ctypes.c_int(0)
-    conv = ctypes.c_int(0)
-    _lib.check(lib.spaimg_solve(ctypes.byref(c), bb.ptr, uu.ptr if uu else None, o.ptr, float(cfg.tol),
-                                int(cfg.max_iters), norms, ctypes.byref(iters), ctypes.byref(conv), stream))
-    k = iters.value
-    hist = [float(norms[i]) for i in range(k + 1)]
+    with s.lock:
+        s.load(b.values, start, stream=stream.value)
+        hist, k, conv = s.run(cfg.tol, cfg.max_iters, stream=stream.value)
+        s.store(out, stream=stream.value)
     rho_hat = (hist[-1] / hist[0]) ** (1.0 / k) if k else float("nan")
-    report = SolveReport(iterations=k, residual_norms=hist, rho_hat=float(rho_hat), converged=bool(conv.value),
+    report = SolveReport(iterations=k, residual_norms=hist, rho_hat=float(rho_hat), converged=conv,
                          wall_time=time.perf_counter() - t0)
     return Grid(b.N, out), report
 
 
 # ------------------------------------------------------------------------------------------
-# persistent solver handle (bench / repeated solves)
+# persistent solver handle (cached by solve/cycle; also the bench / batch API)
 # ------------------------------------------------------------------------------------------
 class Solver:
     """Owns the device level hierarchy and the captured cycle graph for one (cfg, N, dtype)."""
@@ -434,9 +518,12 @@ class Solver:
         self.cfg = cfg
         self.dim = dim
         self.N = N
+        self.device = int(device)
         self.dtype_code = _lib.F32 if dtype in ("float32", "f32", "fp32") else _lib.F64
+        self.shape = (N - 1,) * dim
+        self.lock = threading.Lock()
         self.lib = _lib.load()
-        _lib.check(self.lib.spaimg_set_device(int(device)))
+        _lib.check(self.lib.spaimg_set_device(self.device))
         c, self._keep = _mg_struct(cfg, dim, N, self.dtype_code)
         self._cfg_struct = c
         h = ctypes.c_void_p()
@@ -449,17 +536,17 @@ class Solver:
             self.lib.spaimg_solver_destroy(h)
             self.handle = None
 
-    @staticmethod
-    def _stream(stream):
+    def _stream(self, stream):
         if stream is None:
             import torch
-            return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+            return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
         return ctypes.c_void_p(stream)
 
-    def _ptr(self, values):
+    def _ptr(self, values, out=False):
+        """Validated pointer to an (N-1)^dim array of the solver's dtype on its device or the host."""
         if values is None:
             return None, None
-        a = _Arr(values, self.dtype_code)
+        a = _Arr(values, self.dtype_code, shape=self.shape, out=out, device=self.device)
         return a, a.ptr
 
     def load(self, b_values, u0_values=None, stream=None):
@@ -483,14 +570,14 @@ class Solver:
 
     def solve_batch(self, b_list, u_list, tol=None, max_iters=None, stream=None):
         """Independent zero-start solves of each b in `b_list` into the matching `u_list` array,
-        pipelined so that host<->device copies overlap the solves (pass pinned host tensors or
+        pipelined so that host<->device copies overlap the solves (pass pinned host arrays or
         device tensors).  Returns [(residual_norms, iterations, converged), ...]."""
         if len(b_list) != len(u_list):
             raise ValueError("b_list and u_list must have the same length")
         tol = self.cfg.tol if tol is None else tol
         max_iters = self.cfg.max_iters if max_iters is None else max_iters
         n = len(b_list)
-        keep = [self._ptr(v)[0] for v in list(b_list) + list(u_list)]
+        keep = [self._ptr(v)[0] for v in b_list] + [self._ptr(v, out=True)[0] for v in u_list]
         bp = (ctypes.c_void_p * n)(*[k.ptr for k in keep[:n]])
         up = (ctypes.c_void_p * n)(*[k.ptr for k in keep[n:]])
         norms = (ctypes.c_double * (n * (max_iters + 1)))()
@@ -506,7 +593,7 @@ class Solver:
         return out
 
     def store(self, out_values, stream=None):
-        ok, op = self._ptr(out_values)
+        ok, op = self._ptr(out_values, out=True)
         _lib.check(self.lib.spaimg_solver_store(self.handle, op, self._stream(stream)))
 
     def op(self, which, reps=1, stream=None):
