@@ -11,9 +11,9 @@ the per-cycle residual norm and stop test, exactly the reference solve() loop,
 multigrid.py:206-217).  value = V-cycle DOF/s = unknowns x cycles / step time, whole job.
 
 --impl reference times the reference algorithm on the host CPU (the C restatement in
-oracle/, all host threads; the reference is pure numpy and is not itself shipped to the
-GPU box) on a bounded sample of the same workload: one V(1,1) cycle plus its residual norm
-per step.  Under torchrun only rank 0 runs it.
+oracle/, bitwise equal to the reference, all host threads; the reference is pure numpy and
+is not itself shipped to the GPU box) on the same step: one zero-start solve to tolerance.
+Under torchrun only rank 0 runs it.
 
 Multi-GPU (torchrun, --gpus N): independent replicas, one per GPU (the north star runs
 one problem on one GPU; SURVEY.md §8e "replicas only"); no collective in the data path,
@@ -144,8 +144,19 @@ def barrier(ws):
 # ------------------------------------------------------------------------------------------
 # reference arm: the reference algorithm on host cores
 # ------------------------------------------------------------------------------------------
+def config_dict(ws):
+    """The `config` of the JSON line, identical for both arms."""
+    h = HEADLINE
+    return {"workload": WORKLOADS[h["cfg_id"]][1] + "; step = one solve to tolerance",
+            "l2": "inputs larger than L2 (finest level 134 MB/vector, hierarchy ~0.6 GB)",
+            "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"}
+
+
 def run_reference(args):
-    ws, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    """The reference algorithm on the host cores, same step as our arm: one zero-start solve
+    to tolerance of the workload (the reference solve() loop, multigrid.py:206-217), through the
+    C restatement in oracle/ (bitwise equal to the reference, all host threads)."""
+    ws, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     from oracle import c_oracle, numpy_oracle as npo
@@ -157,26 +168,27 @@ def run_reference(args):
     mt = npo.terms_of(sm.stencil)
     threads = c_oracle.max_threads()
     n0 = (N - 1) ** dim
-    u = np.zeros_like(b)
-    times = []
+    times, cycles = [], []
     for k in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        u = c_oracle.cycle(u, b, N, mt, sm.omega_opt_analytic, h["nu1"], h["nu2"], 1, h["coarsest_N"])
-        c_oracle.residual_norm(u, b, N)
+        u, norms, its, conv = c_oracle.solve_history(b, N, mt, sm.omega_opt_analytic, h["nu1"], h["nu2"], 1,
+                                                     h["coarsest_N"], tol=h["tol"])
         dt = time.perf_counter() - t0
         if k >= args.warmup:
             times.append(dt)
-    t = float(np.mean(times))
-    value = n0 / t
+            cycles.append(its)
+    t = float(np.sum(times))
+    value = n0 * sum(cycles) / t
     cpu = {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-           "sample": f"one {h['smoother']} V({h['nu1']},{h['nu2']}) cycle + residual norm of {h['cfg_id']} "
-                     f"({N - 1}^{dim}, fp64) per step, C restatement of the reference (oracle/), "
-                     f"{threads} OpenMP threads"}
+           "sample": f"one zero-start {h['smoother']} V({h['nu1']},{h['nu2']}) solve to {h['tol']} of {h['cfg_id']} "
+                     f"({N - 1}^{dim}, fp64, {cycles[-1]} cycles + norms) per step, C restatement of the reference "
+                     f"(oracle/), {threads} OpenMP threads"}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[h["cfg_id"]][1], "sample": "1 cycle/step"},
+        "config": config_dict(ws),
+        "cycles_per_solve": float(np.mean(cycles)),
         "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "host_cpu": _cpu_model(), "host_cpus": os.cpu_count(),
@@ -333,9 +345,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOADS[h["cfg_id"]][1] + "; step = one solve to tolerance",
-                       "l2": "inputs larger than L2 (finest level 134 MB/vector, hierarchy ~0.6 GB)",
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+            "config": config_dict(ws),
             "cycles_per_solve": cycles_per_step, "time_to_tol_ms": ms_per_step, "ms_per_cycle": t_cycle * 1e3,
             "bytes_per_cycle": stats["bytes_per_cycle"], "vcycle_gbs": vcycle_gbs,
             "vcycle_roofline_frac": vcycle_gbs / peak, "kernels_per_cycle": stats["kernels_per_cycle"],
@@ -427,6 +437,14 @@ def run_extras(sp, torch, stream, peak):
     except Exception as exc:
         out["configs_1_4_error"] = repr(exc)
     try:
+        out["reference_defaults_W10_cN4"] = w_sweep(sp, torch, stream, peak)
+    except Exception as exc:
+        out["reference_defaults_error"] = repr(exc)
+    try:
+        out["api_solve_host_arrays"] = api_e2e(sp, torch)
+    except Exception as exc:
+        out["api_solve_error"] = repr(exc)
+    try:
         out["config5"] = microbench(sp, torch, stream, peak)
     except Exception as exc:
         out["config5_error"] = repr(exc)
@@ -470,6 +488,82 @@ def config_sweep(sp, torch, stream, peak):
                 "vcycle_roofline_frac": st["bytes_per_cycle"] / (t / k) / 1e9 / peak}
             del so
         del bd
+        torch.cuda.empty_cache()
+    return res
+
+
+def w_sweep(sp, torch, stream, peak):
+    """The reference MgConfig defaults (cycle="W", nu1=1, nu2=0, coarsest_N=4, tol 1e-10;
+    multigrid.py:39-43) on configs 1-4: zero start, resident inputs, time to tolerance and the
+    bytes-moved fraction of a W-cycle (level l visited 2^l times)."""
+    from paper_2206_05543_b200 import workloads
+    res = {}
+    for cfg_id in ("c1", "c2", "c3", "c4"):
+        dim, N, _ = workloads.CONFIGS[cfg_id]
+        bd = torch.as_tensor(workloads.rhs(cfg_id)).to("cuda")
+        sm = "m9" if dim == 2 else "m7"
+        cfg = sp.MgConfig(smoother=sp.named(sm))
+        so = sp.Solver(cfg, dim, N, device=torch.cuda.current_device())
+        so.load(bd)
+        so.run()
+        ts = []
+        for _ in range(3):
+            so.load(None)
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            hist, k, conv = so.run()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(ev0.elapsed_time(ev1) / 1e3)
+        t = float(np.median(ts))
+        st = so.stats()
+        res[f"{cfg_id}/{sm}/W(1,0)/cN4"] = {
+            "cycles": k, "converged": conv, "time_to_tol_ms": t * 1e3, "ms_per_cycle": t / k * 1e3,
+            "dof_per_s": (N - 1) ** dim * k / t, "rho_hat": (hist[-1] / hist[0]) ** (1.0 / k) if k else None,
+            "bytes_per_cycle": st["bytes_per_cycle"], "kernels_per_cycle": st["kernels_per_cycle"],
+            "vcycle_roofline_frac": st["bytes_per_cycle"] / (t / k) / 1e9 / peak}
+        del so, bd
+        torch.cuda.empty_cache()
+    return res
+
+
+def api_e2e(sp, torch):
+    """Wall time of the reference-signature call solve(Grid(N, numpy_b), cfg, u0=0): host
+    arrays in and out (pageable), first call (builds and caches the device hierarchy and
+    graphs) and repeated calls (cached, like the reference's lru_cache on the coarse LU)."""
+    from paper_2206_05543_b200 import workloads
+    from paper_2206_05543_b200.multigrid import clear_solver_cache
+    res = {}
+    for cfg_id, sm in (("c2", "m9"), ("c4", "m7")):
+        dim, N, _ = workloads.CONFIGS[cfg_id]
+        b = workloads.rhs(cfg_id)
+        cfg = sp.MgConfig(smoother=sp.named(sm), cycle="V", nu1=1, nu2=1, coarsest_N=2, tol=1e-10)
+        clear_solver_cache()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        u, rep = sp.solve(sp.Grid(N, b), cfg, u0=0)
+        t_first = time.perf_counter() - t0
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            u, rep = sp.solve(sp.Grid(N, b), cfg, u0=0)
+            ts.append(time.perf_counter() - t0)
+        # the same solve through the persistent handle with device-resident input, for comparison
+        so = sp.cached_solver(cfg, dim, N, 0, torch.cuda.current_device())
+        bd = torch.as_tensor(b).to("cuda")
+        so.load(bd)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        so.load(None)
+        so.run()
+        torch.cuda.synchronize()
+        t_dev = time.perf_counter() - t0
+        res[cfg_id] = {"first_call_s": t_first, "cached_call_s": float(np.median(ts)), "cycles": rep.iterations,
+                       "device_solve_s": t_dev, "bytes_in": b.nbytes, "bytes_out": b.nbytes,
+                       "note": "host numpy b in, host numpy u out (pageable copies included)"}
+        del u, b, bd
+        clear_solver_cache()
         torch.cuda.empty_cache()
     return res
 
