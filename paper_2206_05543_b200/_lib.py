@@ -8,7 +8,11 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libspaimg_cuda.so")
+# SPAIMG_DEBUG=1 selects the checked build (NaN poisoning + barrier jitter; build.py --debug)
+DEBUG = os.environ.get("SPAIMG_DEBUG") == "1"
+LIB_PATH = os.path.join(_PKG, "libspaimg_cuda_debug.so" if DEBUG else "libspaimg_cuda.so")
+# test hook: load another build of the same ABI (the checked-build self-test's fault injection)
+LIB_PATH = os.environ.get("SPAIMG_LIB_OVERRIDE") or LIB_PATH
 
 F64 = 0
 F32 = 1
@@ -104,7 +108,9 @@ def load():
         return _lib
     from . import build as _build
     try:
-        _build.build(force=os.environ.get("SPAIMG_REBUILD") == "1")  # no-op when up to date
+        if os.environ.get("SPAIMG_LIB_OVERRIDE"):
+            raise RuntimeError("prebuilt library requested")
+        _build.build(force=os.environ.get("SPAIMG_REBUILD") == "1", debug=DEBUG)  # no-op when up to date
     except Exception as exc:  # no nvcc / failed build: a prebuilt library is still acceptable
         if not os.path.exists(LIB_PATH):
             raise SpaimgError(f"cannot build the spaimg CUDA library: {exc}") from exc

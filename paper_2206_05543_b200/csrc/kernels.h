@@ -20,6 +20,8 @@ inline cudaError_t launch_k(void (*k)(KP...), dim3 grid, dim3 block, size_t smem
 }
 
 Layout make_layout(int dim, int N, int esize);
+// checked build only: NaN interior and slack, zero two-cell frame (see spaimg_common.cuh)
+template <class T> cudaError_t launch_poison_level(const Layout& L, T* p, cudaStream_t s);
 
 // dense (n^dim, C order) <-> padded interior
 template <class T> cudaError_t launch_pad(const Layout& L, const T* dense, T* padded, cudaStream_t s);

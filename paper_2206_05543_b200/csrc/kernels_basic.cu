@@ -549,9 +549,43 @@ cudaError_t launch_coarse_solve(const Layout& L, const T* b, T* x, const T* lu, 
 }
 
 // ------------------------------------------------------------------------------------------
+// checked build: a level buffer with NaN on its interior and on the slack beyond the two-cell
+// zero frame (the frame itself zero), so every read the algorithm does not define poisons
+// ------------------------------------------------------------------------------------------
+template <class T>
+__global__ void k_poison_level(Layout L, T* p) {
+    const long long lx = L.origin % L.px;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < L.alloc;
+         e += (long long)gridDim.x * blockDim.x) {
+        long long i0, i1, i2 = 0;
+        if (L.dim == 2) {
+            i0 = e / L.px - kGhost;
+            i1 = e % L.px - lx;
+        } else {
+            const long long rem = e % L.pp;
+            i0 = e / L.pp - kGhost;
+            i1 = rem / L.px - kGhost;
+            i2 = rem % L.px - lx;
+        }
+        auto in = [&](long long i, long long lo, long long hi) { return i >= lo && i < hi; };
+        const long long n = L.n;
+        const bool interior = in(i0, 0, n) && in(i1, 0, n) && (L.dim == 2 || in(i2, 0, n));
+        const bool frame = in(i0, -2, n + 2) && in(i1, -2, n + 2) && (L.dim == 2 || in(i2, -2, n + 2));
+        p[e] = (interior || !frame) ? T(__int_as_float(0x7fc00000)) : T(0);
+    }
+}
+
+template <class T>
+cudaError_t launch_poison_level(const Layout& L, T* p, cudaStream_t s) {
+    k_poison_level<T><<<592, 256, 0, s>>>(L, p);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
 // explicit instantiations
 // ------------------------------------------------------------------------------------------
 #define SPAIMG_INST(T)                                                                                          \
+    template cudaError_t launch_poison_level<T>(const Layout&, T*, cudaStream_t);                               \
     template cudaError_t launch_pad<T>(const Layout&, const T*, T*, cudaStream_t);                              \
     template cudaError_t launch_unpad<T>(const Layout&, const T*, T*, cudaStream_t);                            \
     template cudaError_t launch_apply_dense<T>(int, int, const T*, T*, const Terms<T>&, T, cudaStream_t);       \

@@ -64,6 +64,17 @@ __global__ void __launch_bounds__(NT, 1) k_tail(const __grid_constant__ TailArgs
         const TailLv<T>& e = a.lv[0];
         tail_load_entry<T, D>(a, arr, e.x, e.b, e.s0, e.s1);
         for (int i = a.zero_from + t; i < a.arr_elems; i += NT) arr[i] = T(0);
+        if constexpr (kDebugChecks) {
+            // NaN interiors (zero frames) for every array the engine writes before reading
+            __syncthreads();
+            for (int l = 0; l < a.nlv; ++l) {
+                const TailLv<T>& g = a.lv[l];
+                const int F = a.frame;
+                tail_poison<T, D>(arr, g.n, F, g.s0, g.s1, l == 0 ? -1 : g.x);
+                tail_poison<T, D>(arr, g.n, F, g.s0, g.s1, l == 0 ? -1 : g.b);
+                if (g.r >= 0) tail_poison<T, D>(arr, g.n, F, g.s0, g.s1, g.r);
+            }
+        }
         if (nlu > kTailMaxLU) {
             for (int i = t; i < nlu * nlu + 2 * nlu; i += NT) cf[i] = a.coarse_g[i];
             for (int i = t; i < 2 * nlu; i += NT) ci[i] = a.coarse_idx_g[i];
@@ -78,6 +89,7 @@ __global__ void __launch_bounds__(NT, 1) k_tail(const __grid_constant__ TailArgs
         const int type = w & 7, lev = (w >> 3) & 7, nw = (w >> 6) & 31, bw = (w >> 11) & 31, bid = (w >> 16) & 31;
         if (warp >= bw) continue;
         if (i > 0) tail_barrier(bid, bw);
+        SPAIMG_JITTER();
         if (a.prof && t == 0) a.prof[i] = clock64();
         if (warp >= nw) continue;
         if (type == TAIL_COARSE) {

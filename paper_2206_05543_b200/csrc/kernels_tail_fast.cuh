@@ -50,6 +50,8 @@ struct FastTail {
         for (int k = 0; k < l; ++k) c += narr(k) * size(k);
         return c;
     }
+    __device__ static int base_rt(int l) { return base(l); }
+    __device__ static int size_rt(int l) { return size(l); }
     __host__ __device__ static constexpr int xo(int l) { return base(l) + origin(l); }
     __host__ __device__ static constexpr int bo(int l) { return base(l) + size(l) + origin(l); }
     __host__ __device__ static constexpr int ro(int l) { return base(l) + 2 * size(l) + origin(l); }
@@ -97,6 +99,7 @@ struct FastTail {
     __device__ static __forceinline__ void step(const TailArgs<T>& a, int warp, int& pc, Fn&& fn) {
         if (warp < BW) {
             fast_sync<BW>();
+            SPAIMG_JITTER();
             if (a.prof && threadIdx.x == 0) a.prof[pc] = clock64();
             if (warp < NW) fn();
         }
@@ -156,6 +159,18 @@ struct FastTail {
                 visit<L + 1>(a, arr, warp, pc, g == 0, sib && g > 0, sib && g + 1 < a.gamma);
         }
         // prolongation + correction (multigrid.py:184), with the next sweep's residual when one follows
+#ifdef SPAIMG_DEBUG_BREAK_BARRIER
+        // fault injection for the checked-build self-test (tools/README): no barrier before the
+        // prolongation, so it may read the coarse correction before the coarse visit wrote it
+        if constexpr (!fuse_pr(L)) {
+            if (warp < PL) {
+                ++pc;
+                op_prolong<T, D, LW, TL>(f, c, arr);
+            } else {
+                ++pc;
+            }
+        } else
+#endif
         if constexpr (fuse_pr(L)) {
             if (a.nu2 >= 1 || res_next)
                 step<PL, PL>(a, warp, pc, [&] { op_prolong_res<T, D, LW, TL>(f, c, arr); });
@@ -180,6 +195,21 @@ struct FastTail {
         const int t = threadIdx.x;
         tail_load_entry<T, D>(a, arr, xo(0), bo(0), s0(0), s1(0));
         for (int i = zero_from() + t; i < elems(); i += NT) arr[i] = T(0);
+        if constexpr (kDebugChecks) {
+            __syncthreads();
+#pragma unroll 1
+            for (int l = 0; l < NL; ++l) {
+                const int nn = (1 << (LE - l)) - 1, w0 = nn + 2;
+                const int t0 = D == 2 ? w0 : w0 * w0, t1 = D == 3 ? w0 : 0;
+                const int bl = base_rt(l), sz = size_rt(l), org = t0 + t1 + 1;
+                if (l > 0) {
+                    tail_poison<T, D>(arr, nn, 1, t0, t1, bl + org);
+                    tail_poison<T, D>(arr, nn, 1, t0, t1, bl + sz + org);
+                }
+                if (l < NL - 1) tail_poison<T, D>(arr, nn, 1, t0, t1, bl + 2 * sz + org);
+            }
+            for (int i = base(NL) + t; i < elems(); i += NT) arr[i] = T(__int_as_float(0x7fc00000));
+        }
         T* cf = arr + cf_off();
         int* ci = reinterpret_cast<int*>(cf + cf_elems());
         for (int i = t; i < NLU * NLU; i += NT) cf[i] = a.lu[i];

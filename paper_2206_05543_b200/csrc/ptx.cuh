@@ -4,6 +4,8 @@
 
 #include <cstdint>
 
+#include "spaimg_common.cuh"
+
 namespace spaimg {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -24,6 +26,7 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    SPAIMG_JITTER();
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"

@@ -510,6 +510,10 @@ template <class T> struct Solver final : spaimg_solver {
                 if (!fused)  // the unfused residual + relax sweep (stencil radius 2)
                     if (int rc = dalloc(&l.r, (size_t)l.L.alloc)) return rc;
             }
+            if constexpr (kDebugChecks) {
+                for (T* buf : {l.x[0], l.x[1], l.b, l.r})
+                    if (buf) CK(launch_poison_level<T>(l.L, buf, 0));
+            }
             lv.push_back(l);
             if (coarse) break;
             if (N % 2) return fail(SPAIMG_EINVAL, "cannot halve an odd mesh count N=" + std::to_string(N));

@@ -13,6 +13,30 @@
 namespace spaimg {
 
 // ------------------------------------------------------------------------------------------
+// checked build (SPAIMG_DEBUG_CHECKS -> libspaimg_cuda_debug.so, loaded with SPAIMG_DEBUG=1):
+// the in-house stand-in for compute-sanitizer, which is closed on the GPU pool.
+//   * SPAIMG_JITTER(): a random per-warp delay at every synchronisation point of the marching
+//     kernels (mbarrier waits) and the coarse engines (op barriers), so a missing barrier or
+//     wait shows up as a nondeterministic, non-bitwise result;
+//   * level buffers and the engines' shared arrays start with NaN interiors and slack (zero
+//     frames only), so any read before write or outside the stencil's reach poisons a result.
+// ------------------------------------------------------------------------------------------
+#ifdef SPAIMG_DEBUG_CHECKS
+__device__ __forceinline__ void dbg_jitter() {
+    const unsigned c = (unsigned)clock();
+    const unsigned h = (c ^ ((threadIdx.x >> 5) * 0x9E3779B9u) ^ (blockIdx.x * 0x85EBCA6Bu)) * 0xC2B2AE35u;
+    if ((h >> 28) < 6) __nanosleep((h >> 8) & 1023u);
+}
+#define SPAIMG_JITTER() ::spaimg::dbg_jitter()
+constexpr bool kDebugChecks = true;
+#else
+#define SPAIMG_JITTER() \
+    do {                \
+    } while (0)
+constexpr bool kDebugChecks = false;
+#endif
+
+// ------------------------------------------------------------------------------------------
 // rounding-exact scalar ops
 // ------------------------------------------------------------------------------------------
 template <class T> struct Op;

@@ -561,6 +561,21 @@ __device__ __forceinline__ void coarse_fast(const T* cf, const int* ci, const T*
     for (int i = 0; i < NLU; ++i) x[ci[NLU + i]] = y[i];
 }
 
+// checked build: NaN on the interior of one shared-memory level array (origin offset `at`,
+// interior n^D, frame F left at zero); at < 0 skips
+template <class T, int D>
+__device__ __forceinline__ void tail_poison(T* arr, int n, int F, int s0, int s1, int at) {
+    if (at < 0) return;
+    const int cnt = D == 2 ? n * n : n * n * n;
+    for (int q = threadIdx.x; q < cnt; q += NT) {
+        const int i0 = D == 2 ? q / n : q / (n * n);
+        const int rem = D == 2 ? q - i0 * n : q - i0 * n * n;
+        const int i1 = D == 2 ? 0 : rem / n;
+        const int i2 = D == 2 ? rem : rem - i1 * n;
+        arr[at + i0 * s0 + i1 * s1 + i2] = T(__int_as_float(0x7fc00000));
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 // entry level: global padded layout <-> shared memory (frame F, pitches s0, s1)
 // ------------------------------------------------------------------------------------------

@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
-timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; echo bench=$?
-timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo ref=$?
+for v in nojit; do for i in 1 2 3 4 5; do
+  SPAIMG_LIB_OVERRIDE=$PWD/tools/bin/broken/lib_$v.so timeout 600 python tools/sanitize_case.py > gpurun_out/broken_${v}_$i.log 2>&1; echo "$v $i rc=$?"
+done; done
