@@ -41,7 +41,7 @@ extern "C" {
 #define SPAIMG_F32 1
 
 #define SPAIMG_EINVAL (-1)   /* bad argument (shape, N, dim, config) */
-#define SPAIMG_ENOTSUP (-2)  /* stencil radius > 2 in a solver, dtype not supported, ... */
+#define SPAIMG_ENOTSUP (-2)  /* an unsupported request (dtype, engine limits) */
 
 #define SPAIMG_MAX_TERMS 27
 

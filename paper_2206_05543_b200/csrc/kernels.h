@@ -19,7 +19,7 @@ inline cudaError_t launch_k(void (*k)(KP...), dim3 grid, dim3 block, size_t smem
     return cudaLaunchKernelEx(&cfg, k, static_cast<KP>(args)...);
 }
 
-Layout make_layout(int dim, int N, int esize);
+Layout make_layout(int dim, int N, int esize, int ghost = kGhost);
 // checked build only: NaN interior and slack, zero two-cell frame (see spaimg_common.cuh)
 template <class T> cudaError_t launch_poison_level(const Layout& L, T* p, cudaStream_t s);
 

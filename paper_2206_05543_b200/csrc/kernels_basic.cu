@@ -7,6 +7,8 @@
 // spaimg_common.cuh for the cited reference lines.
 #include <cmath>
 
+#include <algorithm>
+
 #include "kernels.h"
 #include "march.cuh"
 
@@ -17,27 +19,29 @@ namespace spaimg {
 // ------------------------------------------------------------------------------------------
 static long long roundup(long long a, long long b) { return (a + b - 1) / b * b; }
 
-Layout make_layout(int dim, int N, int esize) {
+Layout make_layout(int dim, int N, int esize, int ghost) {
     Layout L{};
     L.dim = dim;
     L.N = N;
     L.n = N - 1;
     L.esize = esize;
+    const long long g = ghost < kGhost ? kGhost : ghost;
+    L.ghost = (int)g;
     const long long n = N - 1;
-    const long long LX = 128 / esize;   // interior column 0 is 128-byte aligned
-    const long long V = 16 / esize;     // 16-byte halo granule on the contiguous axis
+    const long long LX = roundup(g, 128 / esize);        // interior column 0 is 128-byte aligned
+    const long long V = std::max<long long>(16 / esize, g);  // right frame: 16-byte halo granule, >= ghost
     if (dim == 2) {
         L.px = roundup(LX + roundup(n, kTileX2D) + V, 32);
-        const long long rows = n + 2 * kGhost;
+        const long long rows = n + 2 * g;
         L.pp = 0;
-        L.origin = kGhost * L.px + LX;
+        L.origin = g * L.px + LX;
         L.alloc = rows * L.px;
     } else {
         L.px = roundup(LX + roundup(n, kTileX3D) + V, 32);
-        const long long ry = kGhost + roundup(n, kTileY3D) + kGhost;
+        const long long ry = g + roundup(n, kTileY3D) + g;
         L.pp = ry * L.px;
-        const long long planes = n + 2 * kGhost;
-        L.origin = kGhost * L.pp + kGhost * L.px + LX;
+        const long long planes = n + 2 * g;
+        L.origin = g * L.pp + g * L.px + LX;
         L.alloc = planes * L.pp;
     }
     return L;
@@ -559,18 +563,19 @@ __global__ void k_poison_level(Layout L, T* p) {
          e += (long long)gridDim.x * blockDim.x) {
         long long i0, i1, i2 = 0;
         if (L.dim == 2) {
-            i0 = e / L.px - kGhost;
+            i0 = e / L.px - L.ghost;
             i1 = e % L.px - lx;
         } else {
             const long long rem = e % L.pp;
-            i0 = e / L.pp - kGhost;
-            i1 = rem / L.px - kGhost;
+            i0 = e / L.pp - L.ghost;
+            i1 = rem / L.px - L.ghost;
             i2 = rem % L.px - lx;
         }
         auto in = [&](long long i, long long lo, long long hi) { return i >= lo && i < hi; };
         const long long n = L.n;
         const bool interior = in(i0, 0, n) && in(i1, 0, n) && (L.dim == 2 || in(i2, 0, n));
-        const bool frame = in(i0, -2, n + 2) && in(i1, -2, n + 2) && (L.dim == 2 || in(i2, -2, n + 2));
+        const long long g = L.ghost;
+        const bool frame = in(i0, -g, n + g) && in(i1, -g, n + g) && (L.dim == 2 || in(i2, -g, n + g));
         p[e] = (interior || !frame) ? T(__int_as_float(0x7fc00000)) : T(0);
     }
 }

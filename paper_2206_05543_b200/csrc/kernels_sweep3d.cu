@@ -54,6 +54,7 @@ struct M3Ctx {
     int n, x0, y0, q0, q_last, z0, z_end, yl, xl, tid;
     bool edge;  // tile touches the right/bottom boundary (masking needed)
     int cx, cy;  // TMA coordinates of the tile's stage origin (x stage)
+    int ghost;   // the layout's ghost planes/rows (TMA coordinate of interior 0)
     // NM == 3 (K2 residual + restriction): coarse output level
     T* cb;
     long long cpx, cpp, corg;
@@ -108,8 +109,8 @@ __device__ __forceinline__ void m3_issue(const M3Ctx<T>& c, const CUtensorMap* x
     constexpr uint32_t xb = G::XR * G::RW * sizeof(T), bb = G::BR * G::RW * sizeof(T);
     fence_proxy_async_smem();
     mbar_arrive_expect_tx(&c.full[slot], FZ ? bb : xb + bb);
-    if (!FZ) tma_load_3d(c.xs + slot * G::XS, xm, c.cx, c.cy, kGhost + q, &c.full[slot]);
-    tma_load_3d(c.bs + slot * G::BS, bm, c.cx, c.cy + 1, kGhost + q, &c.full[slot]);
+    if (!FZ) tma_load_3d(c.xs + slot * G::XS, xm, c.cx, c.cy, c.ghost + q, &c.full[slot]);
+    tma_load_3d(c.bs + slot * G::BS, bm, c.cx, c.cy + 1, c.ghost + q, &c.full[slot]);
 }
 
 // r at a tile-local ring point (ry, rx) of plane j, all operands from shared memory
@@ -333,7 +334,8 @@ __global__ void __launch_bounds__(M3_THREADS, 2)
     c.xl = (threadIdx.x & 31) * VEC;
     c.edge = c.x0 + G::TX > c.n || c.y0 + G::TY > c.n;
     c.cx = (int)(L.origin % L.px) + c.x0 - VEC;  // LX + x0 - VEC
-    c.cy = kGhost + c.y0 - 2;
+    c.ghost = L.ghost;
+    c.cy = c.ghost + c.y0 - 2;
     c.obase = xo + L.origin + (long long)(c.y0 + c.yl) * L.px + c.x0 + c.xl;
 
     if (threadIdx.x == 0) {

@@ -177,8 +177,9 @@ static int store_dense(Scratch& sc, const Layout& L, const T* padded, void* dst,
 }
 
 template <class T>
-static int alloc_level(Scratch& sc, Level<T>& lv, int dim, int N, bool two_x, bool with_b, bool with_r) {
-    lv.L = make_layout(dim, N, sizeof(T));
+static int alloc_level(Scratch& sc, Level<T>& lv, int dim, int N, bool two_x, bool with_b, bool with_r,
+                       int ghost = kGhost) {
+    lv.L = make_layout(dim, N, sizeof(T), ghost);
     lv.sA = (T)hscale(N, -2);
     CK(sc.get(&lv.x[0], (size_t)lv.L.alloc));
     if (two_x) CK(sc.get(&lv.x[1], (size_t)lv.L.alloc));
@@ -248,7 +249,8 @@ static int smooth_t(int dim, int N, const void* u, const void* b, const spaimg_s
     const int rad = stencil_radius(*Ms);
     const int shape = detect_shape(*Ms);
     const bool fused = rad <= 1 && sweep_fused_supported(dim, shape);
-    if (int rc = alloc_level<T>(sc, lv, dim, N, true, true, !fused)) return rc;
+    // the zero frame is as wide as the smoother's reach (stencils.py:139-146)
+    if (int rc = alloc_level<T>(sc, lv, dim, N, true, true, !fused, std::max(kGhost, rad))) return rc;
     lv.sM = (T)hscale(N, Ms->h_exponent);
     if (int rc = load_dense<T>(sc, lv.L, u, lv.x[0], s)) return rc;
     if (steps > 0)
@@ -267,7 +269,6 @@ extern "C" int spaimg_smooth(int dtype, int dim, int N, const void* u, const voi
     if (int rc = check_dims(dtype, dim, N)) return rc;
     if (int rc = check_stencil(M, dim)) return rc;
     if (steps < 0) return fail(SPAIMG_EINVAL, "steps must be non-negative");
-    if (stencil_radius(*M) > kGhost) return fail(SPAIMG_ENOTSUP, "smoother stencil radius > 2 is not supported");
     cudaStream_t s = (cudaStream_t)stream;
     return dtype == SPAIMG_F64 ? smooth_t<double>(dim, N, u, b, M, omega, steps, out, s)
                                : smooth_t<float>(dim, N, u, b, M, omega, steps, out, s);
@@ -495,11 +496,13 @@ template <class T> struct Solver final : spaimg_solver {
         fused = stencil_radius(c.M) <= 1 && sweep_fused_supported(c.dim, shape);
         omega = (T)c.omega;
         k3_flip = ((c.nu1 + c.nu2) & 1) != 0;
-        // levels: halve until N <= coarsest_N (multigrid.py:166, :178)
+        // levels: halve until N <= coarsest_N (multigrid.py:166, :178); the zero frame is as wide
+        // as the smoother's reach (stencils.py:139-146), at least the kernels' two cells
+        const int ghost = std::max(kGhost, stencil_radius(c.M));
         int N = c.N;
         while (true) {
             Level<T> l;
-            l.L = make_layout(c.dim, N, sizeof(T));
+            l.L = make_layout(c.dim, N, sizeof(T), ghost);
             l.sA = (T)hscale(N, -2);
             l.sM = (T)hscale(N, c.M.h_exponent);
             const bool coarse = N <= c.coarsest_N;
@@ -507,7 +510,7 @@ template <class T> struct Solver final : spaimg_solver {
             if (int rc = dalloc(&l.b, (size_t)l.L.alloc)) return rc;
             if (!coarse) {
                 if (int rc = dalloc(&l.x[1], (size_t)l.L.alloc)) return rc;
-                if (!fused)  // the unfused residual + relax sweep (stencil radius 2)
+                if (!fused)  // the unfused residual + relax sweep (stencil radius >= 2)
                     if (int rc = dalloc(&l.r, (size_t)l.L.alloc)) return rc;
             }
             if constexpr (kDebugChecks) {
@@ -748,7 +751,7 @@ template <class T> struct Solver final : spaimg_solver {
         const int thr = tail_threshold(cfg);
         if (thr <= 0) return 0;
         const int F = std::max(1, stencil_radius(cfg.M));
-        if (F > kGhost) return 0;
+        if (F > lv[0].L.ghost) return 0;
         const int nmax = cfg.dim == 2 ? 63 : 15;  // the engine's largest W^dim box
         int dev = 0, optin = 0;
         CK(cudaGetDevice(&dev));
@@ -1345,7 +1348,6 @@ static int check_cfg(const spaimg_mg_config* c) {
     if (c->gamma != 1 && c->gamma != 2) return fail(SPAIMG_EINVAL, "gamma must be 1 (V) or 2 (W)");
     if (c->nu1 < 0 || c->nu2 < 0 || c->nu1 + c->nu2 < 1) return fail(SPAIMG_EINVAL, "need nu1, nu2 >= 0 with nu1 + nu2 >= 1");
     if (c->coarsest_N < 2) return fail(SPAIMG_EINVAL, "coarsest_N must be at least 2");
-    if (stencil_radius(c->M) > kGhost) return fail(SPAIMG_ENOTSUP, "smoother stencil radius > 2 is not supported");
     if (!c->coarse_lu || !c->coarse_piv || c->coarse_n < 1) return fail(SPAIMG_EINVAL, "missing coarse factorisation");
     return 0;
 }

@@ -68,6 +68,7 @@ struct Layout {
     int N;         // mesh count; interior n = N-1 per axis
     int n;
     int esize;     // bytes per element (8 or 4)
+    int ghost;     // zero frame rows/planes on each side (>= kGhost; >= the smoother's radius)
     long long px;  // row pitch (elements)
     long long pp;  // plane pitch (elements), 3D only
     long long origin;  // element offset of interior (0,0[,0])
@@ -78,7 +79,7 @@ struct Layout {
 constexpr int kTileX2D = 512;   // widest 2D strip (columns)
 constexpr int kTileX3D = 128;   // widest 3D tile (columns)
 constexpr int kTileY3D = 32;    // tallest 3D tile (rows)
-constexpr int kGhost = 2;       // ghost rows/planes on the marching axes
+constexpr int kGhost = 2;       // minimum ghost rows/planes (Layout::ghost) on the marching axes
 
 // ------------------------------------------------------------------------------------------
 // stencil term list (entries order of the reference dict, stencils.py:149-151)

@@ -215,7 +215,12 @@ def _custom_stencils(dim):
     far = {o: c for o, c in base.entries.items()}
     far[(2,) + (0,) * (dim - 1)] = Fraction(1, 50)
     far[(0,) * (dim - 1) + (-2,)] = Fraction(1, 40)
-    return {"reversed": (rev, 0.15), "box": (sp.Stencil(dim, box, 2), 0.05), "radius2": (sp.Stencil(dim, far, 2), 0.1)}
+    # radius 3: a wider zero frame on every level (the reference applies any reach, stencils.py:145-146)
+    far3 = dict(far)
+    far3[(-3,) + (0,) * (dim - 1)] = Fraction(1, 60)
+    far3[(0,) * (dim - 1) + (3,)] = Fraction(1, 70)
+    return {"reversed": (rev, 0.15), "box": (sp.Stencil(dim, box, 2), 0.05), "radius2": (sp.Stencil(dim, far, 2), 0.1),
+            "radius3": (sp.Stencil(dim, far3, 2), 0.08)}
 
 
 @pytest.mark.parametrize("dim,N", [(2, 66), (3, 34)])

@@ -1,7 +1,9 @@
-"""Workload for the compute-sanitizer tier (tools/gpu_sanitize.sh): every kernel family of the
-library on small grids, so memcheck / racecheck / synccheck / initcheck runs stay short.
+"""Workload of the sanitizer-substitute tier (tests/test_debug_checks.py, profiles/r02_checked_build.md):
+every kernel family of the library on small grids, run against the checked build
+(SPAIMG_DEBUG=1: NaN-poisoned buffers, jittered barriers).  compute-sanitizer is closed on the
+GPU pool; where it is available, tools/gpu_sanitize.sh runs the same workload under its tools.
 
-    SPAIMG_FLAT_N2=0 SPAIMG_FLAT_N3=0 compute-sanitizer --tool racecheck python tools/sanitize_case.py
+    SPAIMG_DEBUG=1 SPAIMG_FLAT_N2=0 SPAIMG_FLAT_N3=0 python tools/sanitize_case.py
 
 With the flat thresholds at 0 the marching kernels (cp.async.bulk / TMA + mbarrier rings, the
 fused norm, K1+K3, K2 marches) run on every level; with the defaults the flat tile kernels do.
@@ -57,6 +59,16 @@ def check_operators(dim, N):
     S2 = sp.Stencil(dim, far, 2)
     assert np.array_equal(sp.smooth(u, bb, S2, 0.1, 2).values.cpu().numpy(),
                           c_oracle.smooth(x, b, N, npo.terms_of(S2), 0.1, 2))
+    far[(0,) * (dim - 1) + (-3,)] = Fraction(1, 70)  # radius 3: a three-cell frame on every level
+    S3 = sp.Stencil(dim, far, 2)
+    assert np.array_equal(sp.smooth(u, bb, S3, 0.1, 2).values.cpu().numpy(),
+                          c_oracle.smooth(x, b, N, npo.terms_of(S3), 0.1, 2))
+    Nc = 64 if dim == 2 else 16
+    xc = rng.uniform(-1, 1, (Nc - 1,) * dim)
+    bc = rng.uniform(-1, 1, (Nc - 1,) * dim)
+    cfg3 = sp.MgConfig(smoother=S3, omega=0.1, cycle="W", nu1=1, nu2=1, coarsest_N=2)
+    assert np.array_equal(sp.cycle(sp.Grid(Nc, dev(xc)), sp.Grid(Nc, dev(bc)), cfg3).values.cpu().numpy(),
+                          c_oracle.cycle(xc, bc, Nc, npo.terms_of(S3), 0.1, 1, 1, 2, 2))
     assert np.array_equal(sp.residual_restrict(u, bb).values.cpu().numpy(), c_oracle.residual_restrict(x, b, N))
     assert np.array_equal(sp.prolong_correct(u, sp.Grid(N // 2, dev(e))).values.cpu().numpy(),
                           c_oracle.prolong_correct(x, e))
