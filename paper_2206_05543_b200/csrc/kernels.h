@@ -49,6 +49,16 @@ cudaError_t launch_sweep(const Layout& L, const T* x, const T* b, T* xo, const T
 bool sweep_fused_supported(int dim, int shape);
 // K3 + K1: xo = sweep(x + P e) (prolongation + correction fused into the first post-sweep)
 bool sweep_pc_supported(const Layout& L);
+// two smoothing steps in one 2D march (second sweep pipelined three rows behind the first):
+// xo = sweep(sweep(x)) [from_zero: x == 0; no: the input residual's norm], and the K3 variant
+// xo = sweep(sweep(x + P e)); 2D marching levels, named shapes
+bool sweep2_supported(const Layout& L, int shape);
+template <class T>
+cudaError_t launch_sweep2(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, int shape, T sA, T sM,
+                          T omega, bool from_zero, cudaStream_t s, const NormOut* no = nullptr);
+template <class T>
+cudaError_t launch_sweep2_pc(const Layout& L, const Layout& Lc, const T* x, const T* e, const T* b, T* xo,
+                             const Terms<T>& M, int shape, T sA, T sM, T omega, cudaStream_t s);
 template <class T>
 cudaError_t launch_sweep_pc(const Layout& L, const Layout& Lc, const T* x, const T* e, const T* b, T* xo,
                             const Terms<T>& M, int shape, T sA, T sM, T omega, cudaStream_t s);

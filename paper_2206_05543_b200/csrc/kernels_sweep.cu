@@ -125,13 +125,16 @@ __host__ __device__ constexpr int m2_rowlen() { return m2_width<T>() + 2 * m2_ve
 // ring depth: at step j the consumers read coarse rows fl2(j+3)-1 .. fl2(j+3) while the producer
 // stages fl2(j+5), so 4 slots never alias a live row
 constexpr int M2_CR = 4;  // must be a power of 2
+// (TW strips start at c0 = bx (W - 2 VEC) - VEC, so the staged coarse row start is aligned down
+// to a 16-byte boundary and the row is one VEC longer)
 template <class T>
-__host__ __device__ constexpr int m2_crowlen() { return m2_width<T>() / 2 + 2 * m2_vec<T>(); }
+__host__ __device__ constexpr int m2_crowlen(bool two = false) { return m2_width<T>() / 2 + (two ? 3 : 2) * m2_vec<T>(); }
 template <class T>
-constexpr size_t m2_smem_bytes(bool pc = false) {
+constexpr size_t m2_smem_bytes(bool pc = false, bool two = false) {
     return (size_t)2 * M2_ST * m2_rowlen<T>() * sizeof(T)   // x and b stages
            + (size_t)2 * m2_rowlen<T>() * sizeof(T)         // r rows (ring of 2)
-           + (pc ? (size_t)M2_CR * m2_crowlen<T>() * sizeof(T) : 0)  // coarse correction rows
+           + (two ? (size_t)6 * m2_rowlen<T>() * sizeof(T) : 0)  // TW: x' rows (ring of 2), r' rows (ring of 4)
+           + (pc ? (size_t)M2_CR * m2_crowlen<T>(two) * sizeof(T) : 0)  // coarse correction rows
            + (size_t)M2_ST * 8;                             // mbarriers
 }
 
@@ -148,8 +151,13 @@ struct M2Ctx {
     long long px;
     int n, c0, col, sidx, q0, q_last, r0, r_end, lane;
     bool producer, last_strip;
+    // TW: the second sweep's x' rows (ring of 2, horizontal neighbours) and r' rows (ring of 4)
+    T* x1s;
+    T* r2s;
+    int tcons;        // consumer thread index 0 .. W/VEC-1
     // NM == 3: coarse correction e (multigrid.py:184) staged per coarse row
     T* es;            // ring of M2_CR coarse rows
+    int crw;          // coarse row length in the ring (m2_crowlen)
     const T* erow0;   // coarse row 0 at coarse column c0/2 - VEC
     long long epx;
     int m, ce0;       // coarse interior size, first staged coarse column
@@ -164,7 +172,7 @@ __device__ __forceinline__ int fl2(int q) { return q >= 0 ? q / 2 : -((1 - q) / 
 template <class T>
 __device__ __forceinline__ void m2_correct(const M2Ctx<T>& c, T* xrow, int q, int k0, int si) {
     constexpr int VEC = m2_vec<T>();
-    constexpr int CRW = m2_crowlen<T>();
+    const int CRW = c.crw;
     using O = Op<T>;
     auto row = [&](int cr) { return c.es + (cr & (M2_CR - 1)) * CRW - c.ce0; };  // M2_CR: power of 2
     // axis 0: t(J) at coarse columns J0-1 .. J0+VEC/2-1 (J0 = k0/2)
@@ -207,32 +215,43 @@ __device__ __forceinline__ void m2_correct_row(const M2Ctx<T>& c, int q, int slo
     if (t == W / VEC - 1) m2_correct<T>(c, xrow, q, c.c0 + W, VEC + W);
 }
 
-template <class T, int S, bool FZ, int NM = 0>
+template <class T, int S, bool FZ, int NM = 0, bool TW = false>
 __device__ __forceinline__ void m2_issue(const M2Ctx<T>& c, int q, int slot) {
     constexpr int RW = m2_rowlen<T>();
     constexpr uint32_t row_bytes = RW * sizeof(T);
-    constexpr uint32_t crow_bytes = m2_crowlen<T>() * sizeof(T);
+    constexpr uint32_t crow_bytes = m2_crowlen<T>(TW) * sizeof(T);
     // NM == 3: fine row q brings the coarse row floor(q/2) it is the first to need (the first
     // staged row also brings the row below)
     const int ncr = NM == 3 ? ((q & 1) == 0 || q == c.q0 ? 1 : 0) + (q == c.q0 && (q & 1) == 0 ? 1 : 0) : 0;
+    // TW stages rows up to 4 past the chunk; rows beyond the two-row zero frame are loaded from
+    // the frame (their values only feed results forced to zero outside the interior)
+    const int qr = TW ? min(max(q, -kGhost), c.n - 1 + kGhost) : q;
     fence_proxy_async_smem();
     mbar_arrive_expect_tx(&c.full[slot], (FZ ? row_bytes : 2 * row_bytes) + ncr * crow_bytes);
-    if (!FZ) bulk_g2s(c.xs + slot * RW, c.xrow0 + (long long)q * c.px, row_bytes, &c.full[slot]);
-    bulk_g2s(c.bs + slot * RW, c.brow0 + (long long)q * c.px, row_bytes, &c.full[slot]);
+    if (!FZ) bulk_g2s(c.xs + slot * RW, c.xrow0 + (long long)qr * c.px, row_bytes, &c.full[slot]);
+    bulk_g2s(c.bs + slot * RW, c.brow0 + (long long)qr * c.px, row_bytes, &c.full[slot]);
     if constexpr (NM == 3) {
         for (int i = 0; i < ncr; ++i) {
             const int cr = fl2(q) - i;
-            bulk_g2s(c.es + ((cr % M2_CR + M2_CR) % M2_CR) * m2_crowlen<T>(), c.erow0 + (long long)cr * c.epx,
+            const int crr = TW ? min(max(cr, -kGhost), c.m - 1 + kGhost) : cr;
+            bulk_g2s(c.es + ((cr % M2_CR + M2_CR) % M2_CR) * m2_crowlen<T>(TW), c.erow0 + (long long)crr * c.epx,
                      crow_bytes, &c.full[slot]);
         }
     }
 }
 
+// TW (two sweeps in one march): registers of the second sweep, rings indexed by step mod 6/3
+// (r' rows live in shared memory, read back with their neighbours: fewer registers per thread)
+template <class T> struct M2Two {
+    T X1[6][m2_vec<T>()];  // x' rows (own columns)
+    T B[3][m2_vec<T>()];   // b rows (the stage ring has moved on when the second sweep needs them)
+};
+
 // One marching step k (row j = q0 + k): r(j) for the strip (+ halo), then output row j-1.
 // P = k mod 6 makes every stage slot and register-row index a compile-time constant.
-template <class T, int S, bool FZ, int NM, int P>
+template <class T, int S, bool FZ, int NM, int P, bool TW>
 __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_vec<T>()], T (&R)[3][m2_vec<T>()],
-                                        T (&RL)[3], T (&RH)[3], const Terms<T>& M, T sA, T sM, T omega,
+                                        T (&RL)[3], T (&RH)[3], M2Two<T>& tw, const Terms<T>& M, T sA, T sM, T omega,
                                         double& nacc) {
     using O = Op<T>;
     constexpr int VEC = m2_vec<T>();
@@ -249,6 +268,10 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
     if (!c.producer) {
         T bj[VEC];
         V16<T>::ld(c.bs + sj * RW + c.sidx, bj);
+        if constexpr (TW) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) tw.B[P % 3][v] = bj[v];
+        }
         if constexpr (FZ) {
 #pragma unroll
             for (int v = 0; v < VEC; ++v) R[ic][v] = bj[v];  // b - A 0 == b exactly
@@ -263,12 +286,13 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
                 R[ic][v] = residual2d<T>(bj[v], X[ic][v], X[ip][v], X[im][v], xe, xw, sA);
             }
         }
-        if (!row_in || c.last_strip) {
+        if (!row_in || c.last_strip || (TW && c.c0 < 0)) {
 #pragma unroll
             for (int v = 0; v < VEC; ++v)
-                if (!row_in || c.col + v >= c.n) R[ic][v] = T(0);  // r is zero outside the interior
+                if (!row_in || c.col + v >= c.n || (TW && c.col + v < 0)) R[ic][v] = T(0);  // r is zero outside
         }
-        if ((NM == 1 || NM == 2) && j >= c.r0 && j < c.r_end) {
+        // ||r||^2 of own rows (TW: strips overlap by VEC columns; the edge consumers do not count)
+        if ((NM == 1 || NM == 2) && j >= c.r0 && j < c.r_end && (!TW || (c.tcons > 0 && c.tcons < W / VEC - 1))) {
 #pragma unroll
             for (int v = 0; v < VEC; ++v) nacc += (double)R[ic][v] * (double)R[ic][v];  // ||r||^2, own rows
         }
@@ -290,7 +314,7 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
     named_bar_sync(1, (M2_NW + 1) * 32);
     if (c.producer) {
         // stage j-1 was last read before this barrier: refill its slot with row j-1+ST
-        if (c.lane == 0 && j - 1 + ST <= c.q_last) m2_issue<T, S, FZ, NM>(c, j - 1 + ST, sm);
+        if (c.lane == 0 && j - 1 + ST <= c.q_last) m2_issue<T, S, FZ, NM, TW>(c, j - 1 + ST, sm);
         return;
     }
     if (NM == 2) return;
@@ -304,7 +328,7 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
     }
     RL[ic] = rrow[c.sidx - 1];
     RH[ic] = rrow[c.sidx + VEC];
-    if (j - 1 < c.r0) return;
+    if (j - 1 < c.r0 - (TW ? 2 : 0)) return;
     // output row j-1: r rows j-2 (R[ip]), j-1 (R[im]), j (R[ic])
     T out[VEC];
     const int nt = tnt<T, S>(M);
@@ -320,18 +344,80 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
         }
         out[v] = relax<T>(FZ ? T(0) : X[im][v], acc, sM, omega);
     }
-    T* dst = c.orow0 + (long long)(j - 1) * c.px;
-    if (!c.last_strip || c.col + VEC <= c.n) {
-        V16<T>::st(dst, out);
+    if constexpr (!TW) {
+        T* dst = c.orow0 + (long long)(j - 1) * c.px;
+        if (!c.last_strip || c.col + VEC <= c.n) {
+            V16<T>::st(dst, out);
+        } else {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v)
+                if (c.col + v < c.n) dst[v] = out[v];
+        }
     } else {
+        // ---- second sweep (TW), three rows behind the first, bitwise the same trees ----------
+        // x'(j-1): zero outside the interior (the reference's zero extension of the new iterate)
+        constexpr int k1 = (P + 5) % 6, k2 = (P + 4) % 6, k3 = (P + 3) % 6, k4 = (P + 2) % 6;
+        const bool rin1 = (unsigned)(j - 1) < (unsigned)c.n;
 #pragma unroll
         for (int v = 0; v < VEC; ++v)
-            if (c.col + v < c.n) dst[v] = out[v];
+            tw.X1[k1][v] = (rin1 && (unsigned)(c.col + v) < (unsigned)c.n) ? out[v] : T(0);
+        V16<T>::st(c.x1s + ((P + 1) & 1) * RW + c.sidx, tw.X1[k1]);
+        // r'(j-2) = b(j-2) - A x' on rows j-3..j-1 (x'(j-2)'s neighbours: written last step)
+        if (j - 2 >= c.r0 - 1) {
+            T r2[VEC];
+            const T* xr = c.x1s + (P & 1) * RW;
+            const T left = xr[c.sidx - 1], right = xr[c.sidx + VEC];
+            const bool rin2 = (unsigned)(j - 2) < (unsigned)c.n;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+                const T xe = v + 1 < VEC ? tw.X1[k2][v + 1] : right;
+                const T xw = v > 0 ? tw.X1[k2][v - 1] : left;
+                const T rv = residual2d<T>(tw.B[(P + 1) % 3][v], tw.X1[k2][v], tw.X1[k1][v], tw.X1[k3][v], xe, xw, sA);
+                r2[v] = (rin2 && (unsigned)(c.col + v) < (unsigned)c.n) ? rv : T(0);
+            }
+            V16<T>::st(c.r2s + ((j - 2) & 3) * RW + c.sidx, r2);
+        }
+        // x''(j-4) = x'(j-4) + omega (M r') sM from r' rows j-5..j-3 (shared ring, written in the
+        // three previous steps)
+        if (j - 4 >= c.r0 && j - 4 < c.r_end) {
+            T ra[VEC], rb[VEC], rc2[VEC];
+            const T* p5 = c.r2s + ((j - 5) & 3) * RW + c.sidx;
+            const T* p4 = c.r2s + ((j - 4) & 3) * RW + c.sidx;
+            const T* p3 = c.r2s + ((j - 3) & 3) * RW + c.sidx;
+            V16<T>::ld(p5, ra);
+            V16<T>::ld(p4, rb);
+            V16<T>::ld(p3, rc2);
+            const T l5 = p5[-1], l4 = p4[-1], l3 = p3[-1], h5 = p5[VEC], h4 = p4[VEC], h3 = p3[VEC];
+            T out2[VEC];
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+                T acc = T(0);
+#pragma unroll
+                for (int t = 0; t < (S == SHAPE_GENERIC ? kMaxTerms : ShapeT<(S == SHAPE_GENERIC ? 1 : S)>::nt); ++t) {
+                    if (S == SHAPE_GENERIC && t >= nt) break;
+                    const T val = pick<T, VEC>(ra, rb, rc2, l5, l4, l3, h5, h4, h3, toff<T, S>(M, t, 0),
+                                               toff<T, S>(M, t, 1), v);
+                    acc = O::add(acc, O::mul(M.c[t], val));
+                }
+                out2[v] = relax<T>(tw.X1[k4][v], acc, sM, omega);
+            }
+            // strips overlap by VEC columns on each side: the edge consumers only feed their neighbours
+            if (c.tcons > 0 && c.tcons < W / VEC - 1) {
+                T* dst = c.orow0 + (long long)(j - 4) * c.px;
+                if (c.col + VEC <= c.n) {
+                    V16<T>::st(dst, out2);
+                } else {
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v)
+                        if (c.col + v < c.n) dst[v] = out2[v];
+                }
+            }
+        }
     }
 }
 
-template <class T, int S, bool FZ, int NM>
-__global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, const T* __restrict__ x,
+template <class T, int S, bool FZ, int NM, bool TW = false>
+__global__ void __launch_bounds__((M2_NW + 1) * 32, TW ? 3 : 1) k_sweep2d_march(Layout L, const T* __restrict__ x,
                                                                      const T* __restrict__ b, T* __restrict__ xo,
                                                                      Terms<T> M, T sA, T sM, T omega, int rows,
                                                                      NormOut no, const T* __restrict__ e, Layout Lc) {
@@ -344,27 +430,34 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, co
     c.xs = reinterpret_cast<T*>(smem_raw);
     c.bs = c.xs + ST * RW;
     c.rr = c.bs + ST * RW;
-    c.es = c.rr + 2 * RW;
-    c.full = reinterpret_cast<uint64_t*>(c.es + (NM == 3 ? M2_CR * m2_crowlen<T>() : 0));
+    c.x1s = c.rr + 2 * RW;
+    c.r2s = c.x1s + 2 * RW;
+    c.es = c.rr + (TW ? 8 : 2) * RW;
+    c.full = reinterpret_cast<uint64_t*>(c.es + (NM == 3 ? M2_CR * m2_crowlen<T>(TW) : 0));
+    c.crw = m2_crowlen<T>(TW);
     const int warp = threadIdx.x >> 5;
     c.lane = threadIdx.x & 31;
     c.producer = warp == M2_NW;
     c.n = L.n;
     c.px = L.px;
-    c.c0 = blockIdx.x * W;
+    // TW: strips of W columns overlapping by VEC on each side, W - 2 VEC output columns each
+    c.c0 = TW ? (int)blockIdx.x * (W - 2 * VEC) - VEC : (int)blockIdx.x * W;
     c.r0 = blockIdx.y * rows;
     const int r_end = min(c.r0 + rows, c.n);
     c.r_end = r_end;
-    c.q0 = c.r0 - 2;        // first staged row
-    c.q_last = r_end + 1;   // last staged row
+    c.q0 = c.r0 - (TW ? 4 : 2);        // first staged row
+    c.q_last = r_end + (TW ? 4 : 1);   // last staged row
     c.last_strip = c.c0 + W > c.n;
+    c.tcons = (c.producer ? 0 : warp) * 32 + c.lane;
     c.sidx = VEC + (c.producer ? 0 : warp) * 32 * VEC + c.lane * VEC;
     c.col = c.c0 + (c.producer ? 0 : warp) * 32 * VEC + c.lane * VEC;
     c.xrow0 = x + L.origin + (c.c0 - VEC);
     c.brow0 = b + L.origin + (c.c0 - VEC);
     c.orow0 = xo + L.origin + c.col;
     if constexpr (NM == 3) {
-        c.ce0 = c.c0 / 2 - VEC;
+        // first staged coarse column, aligned down to 16 bytes (floor division: c0 < 0 on strip 0)
+        const int ce = c.c0 / 2 - VEC;
+        c.ce0 = TW ? (ce >= 0 ? ce / VEC : -((-ce + VEC - 1) / VEC)) * VEC : ce;
         c.erow0 = e + Lc.origin + c.ce0;
         c.epx = Lc.px;
         c.m = Lc.n;
@@ -376,7 +469,7 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, co
     }
     __syncthreads();
     if (c.producer && c.lane == 0)
-        for (int q = c.q0; q < c.q0 + ST && q <= c.q_last; ++q) m2_issue<T, S, FZ, NM>(c, q, q - c.q0);
+        for (int q = c.q0; q < c.q0 + ST && q <= c.q_last; ++q) m2_issue<T, S, FZ, NM, TW>(c, q, q - c.q0);
 
     T X[3][VEC], R[3][VEC], RL[3], RH[3];
 #pragma unroll
@@ -400,43 +493,46 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32) k_sweep2d_march(Layout L, co
         V16<T>::ld(c.xs + 1 * RW + c.sidx, X[1]);  // x(q0+1) = x(j)
     }
     double nacc = 0.0;
-    const int K = r_end - c.q0;  // steps k = 1 .. K  (rows j = r0-1 .. r_end)
+    M2Two<T> tw;
+    // steps k = 1 .. K: rows j = q0+1 .. r_end (+3 with TW, whose second sweep trails by 3 rows)
+    const int K = r_end + (TW ? 3 : 0) - c.q0;
     for (int kb = 0; kb <= K; kb += ST) {
-        if (kb >= 1) m2_step<T, S, FZ, NM, 0>(c, kb, X, R, RL, RH, M, sA, sM, omega, nacc);
-        if (kb + 1 <= K) m2_step<T, S, FZ, NM, 1>(c, kb + 1, X, R, RL, RH, M, sA, sM, omega, nacc);
-        if (kb + 2 <= K) m2_step<T, S, FZ, NM, 2>(c, kb + 2, X, R, RL, RH, M, sA, sM, omega, nacc);
-        if (kb + 3 <= K) m2_step<T, S, FZ, NM, 3>(c, kb + 3, X, R, RL, RH, M, sA, sM, omega, nacc);
-        if (kb + 4 <= K) m2_step<T, S, FZ, NM, 4>(c, kb + 4, X, R, RL, RH, M, sA, sM, omega, nacc);
-        if (kb + 5 <= K) m2_step<T, S, FZ, NM, 5>(c, kb + 5, X, R, RL, RH, M, sA, sM, omega, nacc);
+        if (kb >= 1) m2_step<T, S, FZ, NM, 0, TW>(c, kb, X, R, RL, RH, tw, M, sA, sM, omega, nacc);
+        if (kb + 1 <= K) m2_step<T, S, FZ, NM, 1, TW>(c, kb + 1, X, R, RL, RH, tw, M, sA, sM, omega, nacc);
+        if (kb + 2 <= K) m2_step<T, S, FZ, NM, 2, TW>(c, kb + 2, X, R, RL, RH, tw, M, sA, sM, omega, nacc);
+        if (kb + 3 <= K) m2_step<T, S, FZ, NM, 3, TW>(c, kb + 3, X, R, RL, RH, tw, M, sA, sM, omega, nacc);
+        if (kb + 4 <= K) m2_step<T, S, FZ, NM, 4, TW>(c, kb + 4, X, R, RL, RH, tw, M, sA, sM, omega, nacc);
+        if (kb + 5 <= K) m2_step<T, S, FZ, NM, 5, TW>(c, kb + 5, X, R, RL, RH, tw, M, sA, sM, omega, nacc);
     }
     if (NM == 1 || NM == 2) norm_epilogue(nacc, no);
 }
 
-template <class T, int S, bool FZ, int NM>
+template <class T, int S, bool FZ, int NM, bool TW = false>
 static cudaError_t launch_sweep2d_march(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA,
                                         T sM, T omega, const NormOut& no, cudaStream_t s, const T* e = nullptr,
                                         const Layout* Lc = nullptr) {
-    constexpr size_t smem = m2_smem_bytes<T>(NM == 3);
+    constexpr size_t smem = m2_smem_bytes<T>(NM == 3, TW);
     if (smem > 48 * 1024) {  // per device, so set on every launch (host-side, cheap)
-        cudaError_t err = cudaFuncSetAttribute(k_sweep2d_march<T, S, FZ, NM>,
+        cudaError_t err = cudaFuncSetAttribute(k_sweep2d_march<T, S, FZ, NM, TW>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (err != cudaSuccess) return err;
     }
     constexpr int threads = (M2_NW + 1) * 32;
     static int occ = 0;
     if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep2d_march<T, S, FZ, NM>, threads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep2d_march<T, S, FZ, NM, TW>, threads, smem);
         if (occ <= 0) occ = 1;
     }
     const int W = m2_width<T>();
-    const int strips = (L.n + W - 1) / W;
+    const int Wout = TW ? W - 2 * m2_vec<T>() : W;
+    const int strips = (L.n + Wout - 1) / Wout;
     const int slots = num_sms() * occ;
-    int chunks = march_chunks(strips, slots, L.n, 16, 4);
+    int chunks = march_chunks(strips, slots, L.n, 16, TW ? 8 : 4);
     const int rows = (L.n + chunks - 1) / chunks;
     chunks = (L.n + rows - 1) / rows;
     dim3 g(strips, chunks);
-    return launch_k(k_sweep2d_march<T, S, FZ, NM>, g, dim3(threads), smem, s, L, x, b, xo, M, sA, sM, omega, rows,
-                      no, e, Lc ? *Lc : L);
+    return launch_k(k_sweep2d_march<T, S, FZ, NM, TW>, g, dim3(threads), smem, s, L, x, b, xo, M, sA, sM, omega,
+                    rows, no, e, Lc ? *Lc : L);
 }
 
 bool sweep_fused_supported(int dim, int shape) {
@@ -520,6 +616,55 @@ cudaError_t launch_sweep_pc(const Layout& L, const Layout& Lc, const T* x, const
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// two smoothing steps in one march (2D marching levels, named shapes): the second sweep runs
+// three rows behind the first inside the same CTA (k_sweep2d_march TW), so x is read and x''
+// written once per pair of sweeps: 24 B per unknown instead of 48.  no != nullptr: the norm of
+// the INPUT residual is appended (part A); the K3 variant applies x + P e first.
+// ------------------------------------------------------------------------------------------
+// Used for the light stencils.  Measured on c2 (4095^2, fp64): jacobi2d V(2,2) 0.545 -> 0.483
+// ms/cycle; the 9-point m9 pair is instruction-issue bound (58 % issue slots busy at 35 % of DRAM
+// bandwidth, 135.8 us per pair against 2 x 66.6 us for two single-sweep marches), so BOX9 keeps
+// one sweep per march and is not instantiated.
+bool sweep2_supported(const Layout& L, int shape) {
+    return L.dim == 2 && L.N > flat_threshold(2) && (shape == SHAPE_C1 || shape == SHAPE_STAR5);
+}
+
+template <class T, int S>
+static cudaError_t sweep2_s(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM, T omega,
+                            bool fz, const NormOut* no, cudaStream_t s) {
+    const NormOut n0{};
+    if (no)
+        return fz ? launch_sweep2d_march<T, S, true, 1, true>(L, x, b, xo, M, sA, sM, omega, *no, s)
+                  : launch_sweep2d_march<T, S, false, 1, true>(L, x, b, xo, M, sA, sM, omega, *no, s);
+    return fz ? launch_sweep2d_march<T, S, true, 0, true>(L, x, b, xo, M, sA, sM, omega, n0, s)
+              : launch_sweep2d_march<T, S, false, 0, true>(L, x, b, xo, M, sA, sM, omega, n0, s);
+}
+
+template <class T>
+cudaError_t launch_sweep2(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, int shape, T sA, T sM,
+                          T omega, bool from_zero, cudaStream_t s, const NormOut* no) {
+    switch (shape) {
+        case SHAPE_C1: return sweep2_s<T, SHAPE_C1>(L, x, b, xo, M, sA, sM, omega, from_zero, no, s);
+        case SHAPE_STAR5: return sweep2_s<T, SHAPE_STAR5>(L, x, b, xo, M, sA, sM, omega, from_zero, no, s);
+        default: return cudaErrorNotSupported;
+    }
+}
+
+template <class T>
+cudaError_t launch_sweep2_pc(const Layout& L, const Layout& Lc, const T* x, const T* e, const T* b, T* xo,
+                             const Terms<T>& M, int shape, T sA, T sM, T omega, cudaStream_t s) {
+    const NormOut none{};
+    switch (shape) {
+        case SHAPE_C1:
+            return launch_sweep2d_march<T, SHAPE_C1, false, 3, true>(L, x, b, xo, M, sA, sM, omega, none, s, e, &Lc);
+        case SHAPE_STAR5:
+            return launch_sweep2d_march<T, SHAPE_STAR5, false, 3, true>(L, x, b, xo, M, sA, sM, omega, none, s, e,
+                                                                       &Lc);
+        default: return cudaErrorNotSupported;
+    }
+}
+
 // residual norm alone through the marching machinery (no smoothing output)
 template <class T>
 cudaError_t launch_norm_march(const Layout& L, const T* x, const T* b, T sA, const NormOut& no, cudaStream_t s) {
@@ -553,6 +698,15 @@ template cudaError_t launch_sweep_pc<double>(const Layout&, const Layout&, const
                                              cudaStream_t);
 template cudaError_t launch_sweep_pc<float>(const Layout&, const Layout&, const float*, const float*, const float*,
                                             float*, const Terms<float>&, int, float, float, float, cudaStream_t);
+template cudaError_t launch_sweep2<double>(const Layout&, const double*, const double*, double*, const Terms<double>&,
+                                           int, double, double, double, bool, cudaStream_t, const NormOut*);
+template cudaError_t launch_sweep2<float>(const Layout&, const float*, const float*, float*, const Terms<float>&, int,
+                                          float, float, float, bool, cudaStream_t, const NormOut*);
+template cudaError_t launch_sweep2_pc<double>(const Layout&, const Layout&, const double*, const double*,
+                                              const double*, double*, const Terms<double>&, int, double, double, double,
+                                              cudaStream_t);
+template cudaError_t launch_sweep2_pc<float>(const Layout&, const Layout&, const float*, const float*, const float*,
+                                             float*, const Terms<float>&, int, float, float, float, cudaStream_t);
 template cudaError_t launch_norm_march<double>(const Layout&, const double*, const double*, double, const NormOut&,
                                                cudaStream_t);
 template cudaError_t launch_norm_march<float>(const Layout&, const float*, const float*, float, const NormOut&,

@@ -257,8 +257,15 @@ static int smooth_t(int dim, int N, const void* u, const void* b, const spaimg_s
         if (int rc = load_dense<T>(sc, lv.L, b, lv.b, s)) return rc;
     const Terms<T> M = to_terms<T>(*Ms);
     int a = 0;
-    for (int k = 0; k < steps; ++k) {
-        if (int rc = do_sweep<T>(lv, a, false, M, shape, fused, (T)omega, s, nullptr)) return rc;
+    for (int k = 0; k < steps;) {
+        // pairs of steps in one march on the 2D marching sizes
+        const bool pair = fused && steps - k >= 2 && sweep2_supported(lv.L, shape);
+        if (pair) {
+            CK(launch_sweep2<T>(lv.L, lv.x[a], lv.b, lv.x[1 - a], M, shape, lv.sA, lv.sM, (T)omega, false, s));
+        } else if (int rc = do_sweep<T>(lv, a, false, M, shape, fused, (T)omega, s, nullptr)) {
+            return rc;
+        }
+        k += pair ? 2 : 1;
         a = 1 - a;
     }
     return store_dense<T>(sc, lv.L, lv.x[a], out, s);
@@ -414,7 +421,6 @@ template <class T> struct Solver final : spaimg_solver {
     int shape = SHAPE_GENERIC;
     bool fused = false;      // fused K1 sweep available for this smoother
     bool fused_norm = false; // norm folded into the first pre-sweep (A) of the next cycle
-    bool k3_flip = false;    // (nu1+nu2) odd: the finest K3 writes the other buffer so a cycle ends in x[0]
     T omega{};
     T* lu = nullptr;
     int* piv = nullptr;
@@ -495,7 +501,6 @@ template <class T> struct Solver final : spaimg_solver {
         shape = detect_shape(c.M);
         fused = stencil_radius(c.M) <= 1 && sweep_fused_supported(c.dim, shape);
         omega = (T)c.omega;
-        k3_flip = ((c.nu1 + c.nu2) & 1) != 0;
         // levels: halve until N <= coarsest_N (multigrid.py:166, :178); the zero frame is as wide
         // as the smoother's reach (stencils.py:139-146), at least the kernels' two cells
         const int ghost = std::max(kGhost, stencil_radius(c.M));
@@ -526,6 +531,10 @@ template <class T> struct Solver final : spaimg_solver {
         if (N != c.coarse_N || count_of(c.dim, N) != c.coarse_n)
             return fail(SPAIMG_EINVAL, "coarse factorisation does not match the coarsest level");
         fused_norm = nsmooth() >= 1 && c.nu1 >= 1 && fused;
+        const char* e2 = getenv("SPAIMG_SWEEP2");
+        pair_sweeps = !(e2 && e2[0] == '0');
+        plan_solve = make_plan(true);
+        plan_cycle = make_plan(false);
         nlu = c.coarse_n;
         std::vector<T> luT(lu_h.begin(), lu_h.end());
         if (int rc = dalloc(&lu, luT.size())) return rc;
@@ -917,10 +926,72 @@ template <class T> struct Solver final : spaimg_solver {
         return 0;
     }
 
+    // ---- pairing smoothing steps into two-sweep marches (launch_sweep2) ---------------------
+    // A pass is one launch writing the other x buffer: one sweep, or two sweeps in one march on
+    // the 2D marching levels (24 B/unknown per pair instead of 48).  Levels >= 1 pair greedily
+    // (visit() returns whichever buffer its result lands in).  Level 0 must end a cycle in x[0]:
+    // its plan picks the most pairs whose pass count is even (a prolongation not fused into a
+    // sweep can also flip, writing the other buffer).
+    struct Level0Plan {
+        int a_sweeps = 0;    // sweeps done by part A (0: no part A in this schedule)
+        int pre_pairs = 0;   // pairs among the remaining pre-sweeps
+        int post_pairs = 0;  // pairs among the post-sweeps (the first one carries the K3 when fused)
+        bool pc = false;     // K3 fused into the first post pass
+        bool k3_flip = false;  // unfused K3 writes the other buffer
+    };
+    Level0Plan plan_solve, plan_cycle;
+    const Level0Plan* plan0 = &plan_cycle;
+
+    bool pair_sweeps = true;  // SPAIMG_SWEEP2=0: one sweep per launch everywhere (comparison knob)
+    bool two_ok(int l) const { return pair_sweeps && fused && sweep2_supported(lv[l].L, shape); }
+
+    Level0Plan make_plan(bool with_a) const {
+        const int nu1 = cfg.nu1, nu2 = cfg.nu2;
+        const bool two0 = nsmooth() >= 1 && two_ok(0);
+        const bool pc_ok = nsmooth() >= 1 && nu2 >= 1 && fused && sweep_pc_supported(lv[0].L);
+        const bool has_a = with_a && fused_norm;
+        Level0Plan best;
+        int best_pairs = -1;
+        for (int a2 = (has_a && two0 && nu1 >= 2) ? 1 : 0; a2 >= 0; --a2) {
+            const int a_sw = has_a ? 1 + a2 : 0;
+            const int r1 = nu1 - a_sw;
+            for (int pp = two0 ? r1 / 2 : 0; pp >= 0; --pp)
+                for (int pc = pc_ok ? 1 : 0; pc >= 0; --pc)
+                    for (int qq = two0 ? nu2 / 2 : 0; qq >= 0; --qq) {
+                        const int passes = (has_a ? 1 : 0) + (r1 - pp) + (nu2 - qq);
+                        const bool flip = !pc && (passes & 1);  // an unfused K3 can fix the parity
+                        if (pc && (passes & 1)) continue;
+                        const int pairs = a2 + pp + qq + (pc ? 1 : 0);
+                        if (pairs > best_pairs) {
+                            best_pairs = pairs;
+                            best.a_sweeps = a_sw;
+                            best.pre_pairs = pp;
+                            best.post_pairs = qq;
+                            best.pc = pc != 0;
+                            best.k3_flip = flip;
+                        }
+                    }
+        }
+        return best;
+    }
+
+    // one pass of `two ? 2 : 1` sweeps on level l: x[a] -> x[1-a]
+    int sweep_pass(int l, int a, bool fz, bool two, cudaStream_t s, int* launches) {
+        Level<T>& L = lv[l];
+        if (two) {
+            if (launch_sweep2<T>(L.L, L.x[a], L.b, L.x[1 - a], M, shape, L.sA, L.sM, omega, fz, s) != cudaSuccess)
+                return -1;
+            ++*launches;
+            return 0;
+        }
+        return do_sweep<T>(L, a, fz, M, shape, fused, omega, s, launches) ? -1 : 0;
+    }
+
     // recursive schedule (multigrid.py:157-185).  Returns the buffer index of level l holding
-    // the result, or -1 on error.  pre_done: the first pre-sweep already ran (level 0: part A;
-    // small 2D levels: fused into the finer level's residual + restriction kernel).
-    int visit(int l, int a, bool fz, cudaStream_t s, int* launches, bool pre_done) {
+    // the result, or -1 on error.  a: the buffer holding the start iterate after the pre_done
+    // pre-sweeps already applied (level 0: part A; small 2D levels: the finer level's residual +
+    // restriction kernel carries the coarse level's first, zero-start sweep).
+    int visit(int l, int a, bool fz, cudaStream_t s, int* launches, int pre_done) {
         if (l >= tail_l && l < nsmooth()) return tail_visit(l, a, fz, s, launches);
         Level<T>& L = lv[l];
         if (l == nsmooth()) {  // u.N <= coarsest_N: direct solve (multigrid.py:166-167)
@@ -928,9 +999,13 @@ template <class T> struct Solver final : spaimg_solver {
             ++*launches;
             return 0;
         }
-        for (int k = 0; k < cfg.nu1; ++k) {
-            if (!(pre_done && k == 0))
-                if (do_sweep<T>(L, a, fz, M, shape, fused, omega, s, launches)) return -1;
+        const bool two = two_ok(l);
+        int pairs = l == 0 ? plan0->pre_pairs : (two ? 1 << 20 : 0);
+        for (int k = pre_done; k < cfg.nu1;) {
+            const bool pair = two && pairs > 0 && cfg.nu1 - k >= 2;
+            if (sweep_pass(l, a, fz, pair, s, launches)) return -1;
+            k += pair ? 2 : 1;
+            pairs -= pair ? 1 : 0;
             a = 1 - a;
             fz = false;
         }
@@ -958,40 +1033,50 @@ template <class T> struct Solver final : spaimg_solver {
             ++*launches;
             c = 0;
         } else {
-            c = visit(l + 1, 0, true, s, launches, rr_fz);
-            for (int g = 1; g < cfg.gamma && c >= 0; ++g) c = visit(l + 1, c, false, s, launches, false);
+            c = visit(l + 1, rr_fz ? 1 : 0, !rr_fz, s, launches, rr_fz ? 1 : 0);
+            for (int g = 1; g < cfg.gamma && c >= 0; ++g) c = visit(l + 1, c, false, s, launches, 0);
             if (c < 0) return -1;
         }
-        const int ao = (l == 0 && k3_flip) ? 1 - a : a;
-        if (cfg.nu2 >= 1 && fused && ao == a && sweep_pc_supported(L.L)) {
-            // prolongation + correction fused into the first post-sweep: x + P e never hits HBM
-            if (launch_sweep_pc<T>(L.L, C.L, L.x[a], C.x[c], L.b, L.x[1 - a], M, shape, L.sA, L.sM, omega, s) !=
-                cudaSuccess)
-                return -1;
+        // post-smoothing; the prolongation + correction (multigrid.py:184) fused into the first
+        // post pass where the level allows it
+        int ppairs = l == 0 ? plan0->post_pairs : (two ? 1 << 20 : 0);
+        const bool pc = l == 0 ? plan0->pc : (cfg.nu2 >= 1 && fused && sweep_pc_supported(L.L));
+        int k = 0;
+        if (pc) {
+            const bool pair = two && ppairs > 0 && cfg.nu2 >= 2;
+            const cudaError_t e =
+                pair ? launch_sweep2_pc<T>(L.L, C.L, L.x[a], C.x[c], L.b, L.x[1 - a], M, shape, L.sA, L.sM, omega, s)
+                     : launch_sweep_pc<T>(L.L, C.L, L.x[a], C.x[c], L.b, L.x[1 - a], M, shape, L.sA, L.sM, omega, s);
+            if (e != cudaSuccess) return -1;
             ++*launches;
             a = 1 - a;
-            for (int k = 1; k < cfg.nu2; ++k) {
-                if (do_sweep<T>(L, a, false, M, shape, fused, omega, s, launches)) return -1;
-                a = 1 - a;
-            }
-            return a;
+            k = pair ? 2 : 1;
+            ppairs -= pair ? 1 : 0;
+        } else {
+            const int ao = (l == 0 && plan0->k3_flip) ? 1 - a : a;
+            if (launch_prolong_correct<T>(L.L, C.L, L.x[a], L.x[ao], C.x[c], s) != cudaSuccess) return -1;
+            ++*launches;
+            a = ao;
         }
-        if (launch_prolong_correct<T>(L.L, C.L, L.x[a], L.x[ao], C.x[c], s) != cudaSuccess) return -1;
-        ++*launches;
-        a = ao;
-        for (int k = 0; k < cfg.nu2; ++k) {
-            if (do_sweep<T>(L, a, false, M, shape, fused, omega, s, launches)) return -1;
+        while (k < cfg.nu2) {
+            const bool pair = two && ppairs > 0 && cfg.nu2 - k >= 2;
+            if (sweep_pass(l, a, false, pair, s, launches)) return -1;
+            k += pair ? 2 : 1;
+            ppairs -= pair ? 1 : 0;
             a = 1 - a;
         }
         return a;
     }
 
-    // A: norm of the iterate in x[0] (+ the first pre-sweep of the next cycle when fused)
+    // A: norm of the iterate in x[0] (+ the first pre-sweep(s) of the next cycle when fused)
     int part_a(cudaStream_t s, int* launches) {
         if (fused_norm) {
             Level<T>& L = lv[0];
             const NormOut no = in_solve_graph ? norm_sink_cond(cur_cond) : norm_sink();
-            CK(launch_sweep<T>(L.L, L.x[0], L.b, L.x[1], M, shape, L.sA, L.sM, omega, false, s, &no));
+            if (plan_solve.a_sweeps == 2)
+                CK(launch_sweep2<T>(L.L, L.x[0], L.b, L.x[1], M, shape, L.sA, L.sM, omega, false, s, &no));
+            else
+                CK(launch_sweep<T>(L.L, L.x[0], L.b, L.x[1], M, shape, L.sA, L.sM, omega, false, s, &no));
             ++*launches;
             return 0;
         }
@@ -1000,7 +1085,9 @@ template <class T> struct Solver final : spaimg_solver {
 
     // B: the rest of the cycle; ends with the iterate back in x[0]
     int part_b(cudaStream_t s, int* launches) {
-        const int out = visit(0, 0, false, s, launches, fused_norm);
+        plan0 = &plan_solve;
+        const int out = visit(0, fused_norm ? 1 : 0, false, s, launches, plan_solve.a_sweeps);
+        plan0 = &plan_cycle;
         if (out != 0) return fail(SPAIMG_EINVAL, out < 0 ? "cycle launch failed: " + g_err : "cycle parity error");
         return 0;
     }
@@ -1083,7 +1170,7 @@ template <class T> struct Solver final : spaimg_solver {
         CK(cudaGraphCreate(&g, 0));
         int launches = 0;
         int rc = capture_into(g, [&](cudaStream_t cs) -> int {
-            const int out = visit(0, 0, false, cs, &launches, false);
+            const int out = visit(0, 0, false, cs, &launches, 0);
             if (out != 0) return fail(SPAIMG_EINVAL, "cycle capture failed: " + g_err);
             return norm_launch(lv[0].x[0], cs, &launches);
         });
@@ -1124,7 +1211,7 @@ template <class T> struct Solver final : spaimg_solver {
                 CK(cudaGraphLaunch(exec_cycle, s));
             } else {
                 int launches = 0;
-                if (visit(0, 0, false, s, &launches, false) != 0) return fail(SPAIMG_EINVAL, "cycle failed: " + g_err);
+                if (visit(0, 0, false, s, &launches, 0) != 0) return fail(SPAIMG_EINVAL, "cycle failed: " + g_err);
                 if (int rc = norm_launch(lv[0].x[0], s, &launches)) return rc;
             }
         }
@@ -1288,6 +1375,9 @@ template <class T> struct Solver final : spaimg_solver {
                 CK(cudaMemsetAsync(slot_d, 0, sizeof(int), s));
                 return part_a(s, &launches);
             }
+            case 5:  // two sweeps in one march (2D marching levels)
+                CK(launch_sweep2<T>(L.L, L.x[0], L.b, L.x[1], M, shape, L.sA, L.sM, omega, false, s));
+                return 0;
             default: return fail(SPAIMG_EINVAL, "unknown op");
         }
     }

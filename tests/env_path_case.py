@@ -23,6 +23,10 @@ CASES = {
     "j2w11": ((2, 128, 6), "jacobi2d", "W", 1, 1, 2),
     "m5v02": ((2, 128, 7), "m5", "V", 0, 2, 4),
     "j3w21": ((3, 32, 8), "jacobi3d", "W", 2, 1, 2),
+    # two-sweep marches: pre/post pairs with odd and even totals (level-0 parity plan)
+    "m9v33": ((2, 2048, 9), "m9", "V", 3, 3, 2),
+    "v9w21": ((2, 1024, 10), "vanka9", "W", 2, 1, 4),
+    "m5v12": ((2, 2048, 11), "m5", "V", 1, 2, 2),
 }
 
 

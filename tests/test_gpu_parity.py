@@ -157,7 +157,7 @@ def test_large_configs_vs_reference_golden(golden_hist, key):
 
 
 @pytest.mark.parametrize("dim,N,sm", [(2, 512, "m9"), (2, 256, "jacobi2d"), (2, 130, "vanka9"), (3, 64, "m7"),
-                                      (3, 34, "jacobi3d")])
+                                      (3, 34, "jacobi3d"), (2, 2050, "jacobi2d"), (2, 2048, "m5")])
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_medium_operators_vs_oracle(dim, N, sm, dtype):
     """Larger, ragged sizes (N-1 odd, tiles partially filled) vs the C oracle, bitwise."""
@@ -170,9 +170,11 @@ def test_medium_operators_vs_oracle(dim, N, sm, dtype):
     M = sp.named(sm)
     mt = npo.terms_of(M.stencil)
     u, bb = sp.Grid(N, dev(x, tdt)), sp.Grid(N, dev(b, tdt))
-    got = host(sp.smooth(u, bb, M.stencil, M.omega_opt_analytic, 2))
-    assert got.dtype == npdt
-    assert np.array_equal(got, c_oracle.smooth(x, b, N, mt, M.omega_opt_analytic, 2, dtype=npdt))
+    # 2 and 3 steps: pairs of steps run as one two-sweep march on the 2D marching sizes (N > 1024)
+    for steps in (2, 3):
+        got = host(sp.smooth(u, bb, M.stencil, M.omega_opt_analytic, steps))
+        assert got.dtype == npdt
+        assert np.array_equal(got, c_oracle.smooth(x, b, N, mt, M.omega_opt_analytic, steps, dtype=npdt)), steps
     assert np.array_equal(host(sp.residual_restrict(u, bb)), c_oracle.residual_restrict(x, b, N, dtype=npdt))
     assert np.array_equal(host(sp.prolong_correct(u, sp.Grid(N // 2, dev(e, tdt)))),
                           c_oracle.prolong_correct(x, e, dtype=npdt))
