@@ -37,7 +37,7 @@ def _fma_counts():
 def _allowed(name):
     if any(k in name for k in ("k_coarse_solve", "k_tail<", "k_tail_fast<", "k_residual_norm")):
         return True
-    m = re.match(r"void spaimg::k_sweep(2d|3d)_march<\w+, \d+, (true|false), (\d)>", name)
+    m = re.match(r"void spaimg::k_sweep(2d|3d)_march<\w+, \d+, (true|false), (\d)(, (true|false))?>", name)
     if m:
         return m.group(3) in ("1", "2")  # norm modes
     return False
