@@ -48,7 +48,7 @@ cudaError_t launch_sweep(const Layout& L, const T* x, const T* b, T* xo, const T
                          T sM, T omega, bool from_zero, cudaStream_t s, const NormOut* no = nullptr);
 bool sweep_fused_supported(int dim, int shape);
 // K3 + K1: xo = sweep(x + P e) (prolongation + correction fused into the first post-sweep)
-bool sweep_pc_supported(const Layout& L);
+bool sweep_pc_supported(const Layout& L, int shape);
 // two smoothing steps in one 2D march (second sweep pipelined three rows behind the first):
 // xo = sweep(sweep(x)) [from_zero: x == 0; no: the input residual's norm], and the K3 variant
 // xo = sweep(sweep(x + P e)); 2D marching levels, named shapes

@@ -542,7 +542,8 @@ bool sweep_fused_supported(int dim, int shape) {
 
 template <class T, int S, bool FZ, int NM>
 cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
-                                 T omega, const NormOut& no, cudaStream_t s, const Layout* Lc = nullptr);
+                                 T omega, const NormOut& no, cudaStream_t s, const Layout* Lc = nullptr,
+                                 const T* ec = nullptr);
 
 template <class T, int S, bool FZ, int NM>
 static cudaError_t sweep_dispatch(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
@@ -599,12 +600,28 @@ cudaError_t launch_sweep(const Layout& L, const T* x, const T* b, T* xo, const T
 // traffic) and a loss on 2048^2, where its extra per-step work is not hidden once the level's
 // HBM time is short.  (A flat-tile fusion for the small levels was measured neutral in 2D and a
 // loss in 3D, and removed.)
-bool sweep_pc_supported(const Layout& L) { return L.dim == 2 && L.N > 2048; }
+// 3D (plane march, named shapes): the prolonged iterate never goes to HBM, 25 B/unknown instead
+// of 17 + 24.  SPAIMG_PC3_N sets the smallest 3D mesh count that uses it (0 turns it off).
+static int pc3_min_n() {
+    const char* e = getenv("SPAIMG_PC3_N");  // read per solver plan (host side, not per launch in a graph)
+    return e ? atoi(e) : 256;
+}
+bool sweep_pc_supported(const Layout& L, int shape) {
+    if (L.dim == 2) return L.N > 2048;
+    return pc3_min_n() > 0 && L.N >= pc3_min_n() && L.N > flat_threshold(3) && (shape == SHAPE_C1 || shape == SHAPE_STAR7);
+}
 
 template <class T>
 cudaError_t launch_sweep_pc(const Layout& L, const Layout& Lc, const T* x, const T* e, const T* b, T* xo,
                             const Terms<T>& M, int shape, T sA, T sM, T omega, cudaStream_t s) {
     const NormOut none{};
+    if (L.dim == 3) {
+        if (shape == SHAPE_C1)
+            return launch_sweep3d_march<T, SHAPE_C1, false, 4>(L, x, b, xo, M, sA, sM, omega, none, s, &Lc, e);
+        if (shape == SHAPE_STAR7)
+            return launch_sweep3d_march<T, SHAPE_STAR7, false, 4>(L, x, b, xo, M, sA, sM, omega, none, s, &Lc, e);
+        return cudaErrorNotSupported;
+    }
     switch (shape) {
         case SHAPE_C1: return launch_sweep2d_march<T, SHAPE_C1, false, 3>(L, x, b, xo, M, sA, sM, omega, none, s, e, &Lc);
         case SHAPE_STAR5:

@@ -40,7 +40,31 @@ template <class T> struct M3 {
     static constexpr int BS = al(BR * RW);
     static constexpr int RS = al(RR * RW);
     static constexpr int NRING = 2 * TX + 2 * TY + 4;
-    static constexpr size_t smem = (size_t)(M3_ST * (XS + BS) + M3_RR * RS) * sizeof(T) + M3_ST * 8;
+    static constexpr int NRP = (NRING + M3_THREADS - 1) / M3_THREADS;  // ring points per thread
+    // NM == 4 (K3 + K1: prolongation + correction fused in front of the sweep): the staged coarse
+    // correction tile, rows [y0/2 - 2, y0/2 + TY/2 + 1), columns [x0/2 - VEC, x0/2 + TX/2 + VEC): the
+    // first column needed is x0/2 - VEC/2 - 1; the tile starts on a 16-byte boundary (TMA box
+    // start addresses that are not 16-byte aligned fault)
+    static constexpr int ECW = TX / 2 + 2 * VEC;   // staged coarse row length (16-byte multiple)
+    static constexpr int ER = TY / 2 + 3;          // staged coarse rows
+    static constexpr int ES = al(ER * ECW);
+    static constexpr int EST = 3;                  // coarse plane ring (indexed by coarse plane mod 3)
+    static __device__ __forceinline__ int eslot(int I) { return (I + 3 * (1 << 20)) % EST; }
+    static constexpr int NHALO = 2 * (TX / VEC + 2) + 2 * (TY / 2);  // 2 x VEC blocks of the x stage's halo
+};
+
+// Shared-memory plan per mode.  The K3 + K1 variant corrects plane j+2 in step j, so three x
+// stages are live and a fourth would leave nothing in flight; instead every thread keeps x(j-1) of
+// its ring point in a register, which frees x(j)'s stage right after step j's barrier: x(j+4) is
+// issued then (two steps of lead, as in the plain sweep).  b(j) is read only in step j and rides
+// with x(j+1) (so the last staged x plane brings the last b needed): three b stages.
+template <class T, int NM> struct M3S {
+    using G = M3<T>;
+    static constexpr bool PC = NM == 4;
+    static constexpr int BST = PC ? 3 : M3_ST;   // b stage ring
+    static constexpr int RRD = M3_RR;            // r plane ring
+    static constexpr size_t smem =
+        (size_t)(M3_ST * G::XS + BST * G::BS + RRD * G::RS + (PC ? G::EST * G::ES : 0)) * sizeof(T) + M3_ST * 8;
 };
 
 template <class T>
@@ -53,12 +77,23 @@ struct M3Ctx {
     long long px, pp;
     int n, x0, y0, q0, q_last, z0, z_end, yl, xl, tid;
     bool edge;  // tile touches the right/bottom boundary (masking needed)
+    // this thread's ring point(s): offset in an r plane / b stage (an x stage: + RW), -1 = none;
+    // inside the interior in-plane
+    int rro[M3<T>::NRP];
+    bool rin[M3<T>::NRP];
     int cx, cy;  // TMA coordinates of the tile's stage origin (x stage)
     int ghost;   // the layout's ghost planes/rows (TMA coordinate of interior 0)
     // NM == 3 (K2 residual + restriction): coarse output level
     T* cb;
     long long cpx, cpp, corg;
     int cm;
+    // NM == 4 (K3 + K1): coarse correction e (multigrid.py:184) staged per coarse plane
+    T* es;
+    int ecx, ecy, eghost;  // TMA coordinates of the staged coarse tile's origin; coarse ghost planes
+    bool pc_edge;          // the tile (with its halo) touches a first/last line of axis 1 or 2
+    // the thread's own block [0] and its halo block [1] (threads < NHALO): tile-local first row /
+    // column, offset in an x stage, offset of coarse (Y-1, X-1) in a staged coarse plane
+    int pry[2], prx[2], pxo[2], peo[2];
 };
 
 // K2 output of coarse plane I = (j-2)/2 from r planes j-2, j-1, j: full weighting along axis 0,
@@ -102,50 +137,197 @@ __device__ __forceinline__ void m3_restrict_out(const M3Ctx<T>& c, int j, const 
     }
 }
 
-template <class T, bool FZ>
-__device__ __forceinline__ void m3_issue(const M3Ctx<T>& c, const CUtensorMap* xm, const CUtensorMap* bm, int q,
-                                         int slot) {
+// stage plane q on full[slot]: x(q) into x slot `slot`, b into its own ring, and (K3 + K1) the
+// coarse correction plane(s) fine plane q is the first to need
+template <class T, bool FZ, int NM>
+__device__ __forceinline__ void m3_issue(const M3Ctx<T>& c, const CUtensorMap* xm, const CUtensorMap* bm,
+                                         const CUtensorMap* em, int q, int slot) {
     using G = M3<T>;
+    using SP = M3S<T, NM>;
     constexpr uint32_t xb = G::XR * G::RW * sizeof(T), bb = G::BR * G::RW * sizeof(T);
+    constexpr uint32_t eb = G::ER * G::ECW * sizeof(T);
+    // K3 + K1: b(q-1) rides with x(q) (x(q) is waited for in step q-2, b(q-1) is read in step q-1
+    // alone); r starts at plane q0+1, so the first two staged planes bring no b
+    const int qb = SP::PC ? q - 1 : q;
+    const bool with_b = !SP::PC || qb > c.q0;
+    const int bslot = SP::PC ? (qb - c.q0 - 1) % 3 : slot;  // b(q0 + 1 + i) in slot i % 3
+    // fine plane q brings the coarse plane floor(q/2) it is the first to need (the first staged
+    // plane also the one below when q is even)
+    const int ncr = SP::PC ? ((q & 1) == 0 || q == c.q0 ? 1 : 0) + (q == c.q0 && (q & 1) == 0 ? 1 : 0) : 0;
     fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&c.full[slot], FZ ? bb : xb + bb);
+    mbar_arrive_expect_tx(&c.full[slot], (FZ ? 0 : xb) + (with_b ? bb : 0) + ncr * eb);
     if (!FZ) tma_load_3d(c.xs + slot * G::XS, xm, c.cx, c.cy, c.ghost + q, &c.full[slot]);
-    tma_load_3d(c.bs + slot * G::BS, bm, c.cx, c.cy + 1, c.ghost + q, &c.full[slot]);
+    if (with_b) tma_load_3d(c.bs + bslot * G::BS, bm, c.cx, c.cy + 1, c.ghost + qb, &c.full[slot]);
+    if constexpr (SP::PC) {
+        for (int i = 0; i < ncr; ++i) {
+            const int I = (q >> 1) - i;  // arithmetic shift: floor(q/2)
+            tma_load_3d(c.es + G::eslot(I) * G::ES, em, c.ecx, c.ecy, c.eghost + I, &c.full[slot]);
+        }
+    }
 }
 
-// r at a tile-local ring point (ry, rx) of plane j, all operands from shared memory
-template <class T, bool FZ>
-__device__ __forceinline__ T m3_ring_r(const M3Ctx<T>& c, int sj, int sp, int sm, int ry, int rx, int j, T sA) {
+// K3 + K1: x(q, .) += (P e)(q, .) on the 2 x VEC block of the staged x plane at tile-local fine
+// rows ry, ry+1 (ry even, -2 .. TY) and columns rx .. rx+VEC-1 (rx a multiple of VEC, -VEC .. TX):
+// separable d-linear interpolation, axis 0 first, then 1, then 2, with the reference end formulas
+// (multigrid.py:122-144) -- the k_prolong_correct3d tree.  Outside the interior P e is exactly 0
+// (zero frames), so the halo of a boundary tile stays 0.  EDGE = false: no first/last line of
+// any axis is involved (warp-uniform fast path, no selects).
+template <class T, bool EDGE>
+__device__ __forceinline__ void m3_correct(const M3Ctx<T>& c, T* xr, const T* em, const T* e0, int q, int ry, int rx) {
     using G = M3<T>;
-    const int gy = c.y0 + ry, gx = c.x0 + rx;
-    if ((unsigned)j >= (unsigned)c.n || (unsigned)gy >= (unsigned)c.n || (unsigned)gx >= (unsigned)c.n) return T(0);
-    const T b = c.bs[sj * G::BS + (ry + 1) * G::RW + G::VEC + rx];
+    using O = Op<T>;
+    constexpr int VEC = G::VEC, C = VEC / 2, ECW = G::ECW;
+    const int m = c.cm;
+    // em / e0: the staged coarse planes floor(q/2) - 1 and floor(q/2) at coarse (Y-1, X-1) of the
+    // block's first cell
+    T t[2][C + 1];
+    if (q & 1) {
+#pragma unroll
+        for (int d = 0; d < 2; ++d)
+#pragma unroll
+            for (int i = 0; i <= C; ++i) t[d][i] = e0[d * ECW + i];
+    } else {
+        const int I = q >> 1;
+        const bool fI = EDGE && I == 0, lI = EDGE && I == m;
+#pragma unroll
+        for (int d = 0; d < 2; ++d)
+#pragma unroll
+            for (int i = 0; i <= C; ++i) t[d][i] = pl_even<T>(em[d * ECW + i], e0[d * ECW + i], fI, lI);
+    }
+    const int J = (c.y0 + ry) >> 1, K0 = (c.x0 + rx) >> 1;
+    const bool fJ = EDGE && J == 0, lJ = EDGE && J == m;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        T u[C + 1];
+#pragma unroll
+        for (int i = 0; i <= C; ++i) u[i] = h ? t[1][i] : pl_even<T>(t[0][i], t[1][i], fJ, lJ);
+        T xv[VEC];
+        V16<T>::ld(xr + h * G::RW, xv);
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+            const int K = K0 + i;
+            xv[2 * i] = O::add(xv[2 * i], pl_even<T>(u[i], u[i + 1], EDGE && K == 0, EDGE && K == m));
+            xv[2 * i + 1] = O::add(xv[2 * i + 1], u[i + 1]);
+        }
+        V16<T>::st(xr + h * G::RW, xv);
+    }
+}
+
+// tile-local (first row, first column) of halo block h of the x stage (0 .. NHALO-1)
+template <class T>
+__device__ __forceinline__ void m3_halo_block(int h, int& ry, int& rx) {
+    using G = M3<T>;
+    constexpr int VEC = G::VEC, NBX = G::TX / VEC + 2;
+    if (h < 2 * NBX) {
+        ry = h < NBX ? -2 : G::TY;
+        rx = ((h < NBX ? h : h - NBX) - 1) * VEC;
+    } else {
+        const int g = h - 2 * NBX;
+        ry = (g % (G::TY / 2)) * 2;
+        rx = g < G::TY / 2 ? -VEC : G::TX;
+    }
+}
+
+// the whole staged x plane q in `slot`, in place: every thread its own 2 x VEC block, the first
+// NHALO threads also one block of the halo frame (a rolled two-pass loop keeps the unrolled march
+// small; the blocks' stage offsets are per-thread constants, M3Ctx::pxo / peo)
+// es0: the ring slot of coarse plane floor(q/2) (the plane an odd q copies, the upper plane of an
+// even q); the plane below is one slot back
+template <class T>
+__device__ __forceinline__ void m3_correct_plane(const M3Ctx<T>& c, int q, int slot, int es0) {
+    using G = M3<T>;
+    T* xpl = c.xs + slot * G::XS;
+    // first/last lines: coarse plane 0 / m on even fine planes, and the tile's own edge flag
+    const bool edge = c.pc_edge || q <= 0 || q >= 2 * c.cm;
+    const T* e0 = c.es + es0 * G::ES;
+    const T* em = c.es + (es0 == 0 ? G::EST - 1 : es0 - 1) * G::ES;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+        if (pass && c.tid >= G::NHALO) break;
+        // (selects, not indexing: a runtime index would put the context in local memory)
+        const int xo = pass ? c.pxo[1] : c.pxo[0], eo = pass ? c.peo[1] : c.peo[0];
+        if (edge)
+            m3_correct<T, true>(c, xpl + xo, em + eo, e0 + eo, q, pass ? c.pry[1] : c.pry[0], pass ? c.prx[1] : c.prx[0]);
+        else
+            m3_correct<T, false>(c, xpl + xo, em + eo, e0 + eo, q, 0, 0);
+    }
+    fence_proxy_async_smem();  // the slot is refilled by TMA later
+}
+
+// r at a tile-local ring point (ry, rx) of plane j, all operands from shared memory.  CACHE (K3 +
+// K1): x(j-1) at the point comes from `prev` (this thread read it as x(j) a step ago), so x(j-1)'s
+// stage is not touched; prev is then advanced to x(j).
+template <class T, bool FZ, bool CACHE>
+__device__ __forceinline__ T m3_ring_r(const M3Ctx<T>& c, int sj, int sp, int sm, int sb, int ro, bool in, int j, T sA,
+                                       T& prev) {
+    using G = M3<T>;
+    const bool out = (unsigned)j >= (unsigned)c.n || !in;
+    if (!CACHE && out) return T(0);
+    const T b = c.bs[sb * G::BS + ro];
     if constexpr (FZ) {
         return b;
     } else {
-        const T* xj = c.xs + sj * G::XS + (ry + 2) * G::RW + G::VEC + rx;
-        const T xp0 = c.xs[sp * G::XS + (ry + 2) * G::RW + G::VEC + rx];
-        const T xm0 = c.xs[sm * G::XS + (ry + 2) * G::RW + G::VEC + rx];
-        return residual3d<T>(b, xj[0], xp0, xm0, xj[G::RW], xj[-G::RW], xj[1], xj[-1], sA);
+        const T* xj = c.xs + sj * G::XS + G::RW + ro;
+        const T xp0 = c.xs[sp * G::XS + G::RW + ro];
+        T xm0;
+        if constexpr (CACHE) {
+            xm0 = prev;
+            prev = xj[0];
+        } else {
+            xm0 = c.xs[sm * G::XS + G::RW + ro];
+        }
+        const T r = residual3d<T>(b, xj[0], xp0, xm0, xj[G::RW], xj[-G::RW], xj[1], xj[-1], sA);
+        return (CACHE && out) ? T(0) : r;
+    }
+}
+
+// tile-local coordinates of ring point i (0 .. NRING-1): consecutive threads take consecutive
+// points, so the top/bottom ring rows are read as contiguous shared-memory runs
+template <class T>
+__device__ __forceinline__ void m3_ring_pt(int i, int& ry, int& rx) {
+    using G = M3<T>;
+    if (i < G::TX) {
+        ry = -1, rx = i;
+    } else if (i < 2 * G::TX) {
+        ry = G::TY, rx = i - G::TX;
+    } else if (i < 2 * G::TX + G::TY) {
+        ry = i - 2 * G::TX, rx = -1;
+    } else if (i < 2 * G::TX + 2 * G::TY) {
+        ry = i - 2 * G::TX - G::TY, rx = G::TX;
+    } else {
+        const int q = i - 2 * G::TX - 2 * G::TY;
+        ry = (q & 2) ? G::TY : -1;
+        rx = (q & 1) ? G::TX : -1;
     }
 }
 
 template <class T, int S, bool FZ, int NM, int P>
-__device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xmap, const CUtensorMap* bmap, int k,
-                                        T (&X)[3][2][M3<T>::VEC], T (&R)[3][2][M3<T>::VEC], const Terms<T>& M,
+__device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xmap, const CUtensorMap* bmap,
+                                        const CUtensorMap* emap, int k, T (&X)[3][2][M3<T>::VEC],
+                                        T (&R)[3][2][M3<T>::VEC], T (&XP)[M3<T>::NRP], int& ecs, const Terms<T>& M,
                                         T sA, T sM, T omega, double& nacc) {
     using G = M3<T>;
+    using SP = M3S<T, NM>;
     using O = Op<T>;
+    constexpr bool PC = SP::PC;
+    static_assert(!PC || (S != SHAPE_GENERIC && !FZ), "K3 + K1: named shapes, a given iterate");
     constexpr int VEC = G::VEC;
     constexpr int RW = G::RW;
     constexpr int sj = P % M3_ST, sp = (P + 1) % M3_ST, sm = (P + M3_ST - 1) % M3_ST;
+    constexpr int bj_slot = PC ? (P + 2) % 3 : P % M3_ST;  // b(j): K3 + K1 stages b(q0 + 1 + i) in slot i % 3
     constexpr int ic = P % 3, ip = (P + 1) % 3, im = (P + 2) % 3;
-    constexpr int rj = P % M3_RR, rj1 = (P + 2) % M3_RR, rj2 = (P + 1) % M3_RR;  // r ring: planes j, j-1, j-2
+    // r ring: planes j, j-1, j-2 (the two-plane ring of the K3 + K1 variant never reads r(j-2))
+    constexpr int rj = P % SP::RRD, rj1 = (P + SP::RRD - 1) % SP::RRD, rj2 = (P + 1) % SP::RRD;
     const int j = c.q0 + k;
     // generic shapes read r(j-3)'s ring slot in the previous step's output phase
     // (NM == 3 reads r(j-3)'s slot as r(j-2) in its output phase)
     if constexpr (S == SHAPE_GENERIC || NM == 3) __syncthreads();
-    mbar_wait(&c.full[sp], (uint32_t)(((k + 1) / M3_ST) & 1));
+    if constexpr (PC) {
+        // plane j+1 arrived (and was corrected) a step ago; plane j+2 is corrected in this step
+        if (j + 2 <= c.q_last) mbar_wait(&c.full[(P + 2) % M3_ST], (uint32_t)(((k + 2) / M3_ST) & 1));
+    } else {
+        mbar_wait(&c.full[sp], (uint32_t)(((k + 1) / M3_ST) & 1));
+    }
     const bool plane_in = (unsigned)j < (unsigned)c.n;
 
     // ---- r(j) at the two owned rows -------------------------------------------------------
@@ -154,7 +336,7 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
     for (int yy = 0; yy < 2; ++yy) {
         const int row = c.yl + yy;
         T bj[VEC];
-        V16<T>::ld(c.bs + sj * G::BS + (row + 1) * RW + VEC + c.xl, bj);
+        V16<T>::ld(c.bs + bj_slot * G::BS + (row + 1) * RW + VEC + c.xl, bj);
         if constexpr (FZ) {
 #pragma unroll
             for (int v = 0; v < VEC; ++v) R[ic][yy][v] = bj[v];
@@ -197,32 +379,25 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
     }
     // ---- r(j) on the one-point ring of the tile, spread over all warps ------------------------
     if (NM != 2) {
-        // consecutive threads take consecutive ring points, so the top/bottom ring rows are read
-        // as contiguous shared-memory runs
 #pragma unroll
-        for (int base = 0; base < G::NRING; base += M3_THREADS) {
-            const int i = base + c.tid;
-            if (i < G::NRING) {
-                int ry, rx;
-                if (i < G::TX) {
-                    ry = -1, rx = i;
-                } else if (i < 2 * G::TX) {
-                    ry = G::TY, rx = i - G::TX;
-                } else if (i < 2 * G::TX + G::TY) {
-                    ry = i - 2 * G::TX, rx = -1;
-                } else if (i < 2 * G::TX + 2 * G::TY) {
-                    ry = i - 2 * G::TX - G::TY, rx = G::TX;
-                } else {
-                    const int q = i - 2 * G::TX - 2 * G::TY;
-                    ry = (q & 2) ? G::TY : -1;
-                    rx = (q & 1) ? G::TX : -1;
-                }
-                rpl[(ry + 1) * RW + VEC + rx] = m3_ring_r<T, FZ>(c, sj, sp, sm, ry, rx, j, sA);
-            }
+        for (int i = 0; i < G::NRP; ++i) {
+            if (c.rro[i] >= 0)
+                rpl[c.rro[i]] = m3_ring_r<T, FZ, PC>(c, sj, sp, sm, bj_slot, c.rro[i], c.rin[i], j, sA, XP[i]);
         }
     }
+    if constexpr (PC) {
+        // x + P e on the staged plane j+2 (tile and halo), in place, a step before anything reads
+        // it: independent of the r(j) work above, ordered before the next step by the barrier below
+        if (j + 2 <= c.q_last) m3_correct_plane<T>(c, j + 2, (P + 2) % M3_ST, ecs);
+        // ecs follows floor(q/2) mod EST of the plane corrected next
+        if (j & 1) ecs = ecs == G::EST - 1 ? 0 : ecs + 1;
+    }
     __syncthreads();
-    if (c.tid == 0 && j - 1 + M3_ST <= c.q_last) m3_issue<T, FZ>(c, xmap, bmap, j - 1 + M3_ST, sm);
+    if constexpr (PC) {  // x(j) is dead from here on (see M3S): its stage takes x(j+4)
+        if (c.tid == 0 && j + M3_ST <= c.q_last) m3_issue<T, FZ, NM>(c, xmap, bmap, emap, j + M3_ST, sj);
+    } else {
+        if (c.tid == 0 && j - 1 + M3_ST <= c.q_last) m3_issue<T, FZ, NM>(c, xmap, bmap, emap, j - 1 + M3_ST, sm);
+    }
     if constexpr (NM == 3) {
         if ((j & 1) == 0 && j >= c.z0 + 1)
             m3_restrict_out<T>(c, j, c.rr + rj * G::RS, c.rr + rj1 * G::RS, c.rr + rj2 * G::RS, R[ic], R[im], R[ip]);
@@ -298,16 +473,18 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
 template <class T, int S, bool FZ, int NM>
 __global__ void __launch_bounds__(M3_THREADS, 2)
     k_sweep3d_march(Layout L, const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap bmap,
-                    const T* __restrict__ x, T* __restrict__ xo, Terms<T> M, T sA, T sM, T omega, int planes,
-                    NormOut no, Layout Lc) {
+                    const __grid_constant__ CUtensorMap emap, const T* __restrict__ x, T* __restrict__ xo, Terms<T> M,
+                    T sA, T sM, T omega, int planes, NormOut no, Layout Lc) {
     using G = M3<T>;
+    using SP = M3S<T, NM>;
     constexpr int VEC = G::VEC;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     M3Ctx<T> c;
     c.xs = reinterpret_cast<T*>(smem_raw);
     c.bs = c.xs + M3_ST * G::XS;
-    c.rr = c.bs + M3_ST * G::BS;
-    c.full = reinterpret_cast<uint64_t*>(c.rr + M3_RR * G::RS);
+    c.rr = c.bs + SP::BST * G::BS;
+    c.es = c.rr + SP::RRD * G::RS;
+    c.full = reinterpret_cast<uint64_t*>(c.es + (SP::PC ? G::EST * G::ES : 0));
     c.tid = threadIdx.x;
     c.n = L.n;
     c.px = L.px;
@@ -333,20 +510,47 @@ __global__ void __launch_bounds__(M3_THREADS, 2)
     c.yl = (threadIdx.x >> 5) * 2;
     c.xl = (threadIdx.x & 31) * VEC;
     c.edge = c.x0 + G::TX > c.n || c.y0 + G::TY > c.n;
+#pragma unroll
+    for (int i = 0; i < G::NRP; ++i) {
+        const int p = i * M3_THREADS + (int)threadIdx.x;
+        int ry = 0, rx = 0;
+        m3_ring_pt<T>(p, ry, rx);
+        c.rro[i] = p < G::NRING ? (ry + 1) * G::RW + VEC + rx : -1;
+        c.rin[i] = (unsigned)(c.y0 + ry) < (unsigned)c.n && (unsigned)(c.x0 + rx) < (unsigned)c.n;
+    }
     c.cx = (int)(L.origin % L.px) + c.x0 - VEC;  // LX + x0 - VEC
     c.ghost = L.ghost;
     c.cy = c.ghost + c.y0 - 2;
     c.obase = xo + L.origin + (long long)(c.y0 + c.yl) * L.px + c.x0 + c.xl;
+    if constexpr (SP::PC) {
+        c.cm = Lc.n;
+        c.eghost = Lc.ghost;
+        c.ecx = (int)(Lc.origin % Lc.px) + (c.x0 >> 1) - VEC;
+        c.ecy = Lc.ghost + (c.y0 >> 1) - 2;
+        c.pc_edge = c.y0 == 0 || c.x0 == 0 || ((c.y0 + G::TY) >> 1) >= Lc.n || ((c.x0 + G::TX + VEC) >> 1) >= Lc.n;
+        c.pry[0] = c.yl;
+        c.prx[0] = c.xl;
+        c.pry[1] = c.prx[1] = 0;
+        if (c.tid < G::NHALO) m3_halo_block<T>(c.tid, c.pry[1], c.prx[1]);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            c.pxo[i] = (c.pry[i] + 2) * G::RW + VEC + c.prx[i];
+            // staged coarse tile: row 0 = coarse row y0/2 - 2, column 0 = coarse column x0/2 - VEC
+            c.peo[i] = ((c.pry[i] >> 1) + 1) * G::ECW + (c.prx[i] >> 1) + VEC - 1;
+        }
+    }
 
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&xmap);
         tma_prefetch_desc(&bmap);
+        if (SP::PC) tma_prefetch_desc(&emap);
         for (int i = 0; i < M3_ST; ++i) mbar_init(&c.full[i], 1);
         mbar_fence_init();
     }
     __syncthreads();
     if (threadIdx.x == 0)
-        for (int q = c.q0; q < c.q0 + M3_ST && q <= c.q_last; ++q) m3_issue<T, FZ>(c, &xmap, &bmap, q, q - c.q0);
+        for (int q = c.q0; q < c.q0 + M3_ST && q <= c.q_last; ++q)
+            m3_issue<T, FZ, NM>(c, &xmap, &bmap, &emap, q, q - c.q0);
 
     T X[3][2][VEC], R[3][2][VEC];
 #pragma unroll
@@ -357,6 +561,20 @@ __global__ void __launch_bounds__(M3_THREADS, 2)
             for (int v = 0; v < VEC; ++v) X[a][yy][v] = R[a][yy][v] = T(0);
     mbar_wait(&c.full[0], 0);
     mbar_wait(&c.full[1], 0);
+    T XP[G::NRP];
+#pragma unroll
+    for (int i = 0; i < G::NRP; ++i) XP[i] = T(0);
+    if constexpr (SP::PC) {  // planes q0 .. q0+2 corrected before the march (then two planes ahead)
+        m3_correct_plane<T>(c, c.q0, 0, G::eslot(c.q0 >> 1));
+        m3_correct_plane<T>(c, c.q0 + 1, 1, G::eslot((c.q0 + 1) >> 1));
+        mbar_wait(&c.full[2], 0);
+        m3_correct_plane<T>(c, c.q0 + 2, 2, G::eslot((c.q0 + 2) >> 1));
+        __syncthreads();
+        // x(q0) at this thread's ring point(s): x(j-1) of the first step
+#pragma unroll
+        for (int i = 0; i < G::NRP; ++i)
+            if (c.rro[i] >= 0) XP[i] = c.xs[G::RW + c.rro[i]];
+    }
     if (!FZ) {
 #pragma unroll
         for (int yy = 0; yy < 2; ++yy) {
@@ -364,12 +582,17 @@ __global__ void __launch_bounds__(M3_THREADS, 2)
             V16<T>::ld(c.xs + 1 * G::XS + (c.yl + yy + 2) * G::RW + VEC + c.xl, X[1][yy]);
         }
     }
+    if constexpr (SP::PC) {  // every read of x(q0)'s stage is done: it takes x(q0 + 4)
+        __syncthreads();
+        if (threadIdx.x == 0 && c.q0 + M3_ST <= c.q_last) m3_issue<T, FZ, NM>(c, &xmap, &bmap, &emap, c.q0 + M3_ST, 0);
+    }
     double nacc = 0.0;
+    int ecs = SP::PC ? G::eslot((c.q0 + 3) >> 1) : 0;  // step k = 1 corrects plane q0 + 3
     const int K = z_end - c.q0;  // steps k = 1..K (planes j = z0-1 .. z_end)
     for (int kb = 0; kb <= K; kb += 12) {
 #define M3STEP(p)                                                                            \
     if (kb + (p) >= 1 && kb + (p) <= K)                                                     \
-        m3_step<T, S, FZ, NM, (p)>(c, &xmap, &bmap, kb + (p), X, R, M, sA, sM, omega, nacc);
+        m3_step<T, S, FZ, NM, (p)>(c, &xmap, &bmap, &emap, kb + (p), X, R, XP, ecs, M, sA, sM, omega, nacc);
         M3STEP(0) M3STEP(1) M3STEP(2) M3STEP(3) M3STEP(4) M3STEP(5)
         M3STEP(6) M3STEP(7) M3STEP(8) M3STEP(9) M3STEP(10) M3STEP(11)
 #undef M3STEP
@@ -394,12 +617,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 3-D map over a whole padded level allocation (cols, rows, planes), box = (RW, rows, 1)
 template <class T>
-static cudaError_t make_map(CUtensorMap* map, const Layout& L, const T* base, int box_rows) {
+static cudaError_t make_map(CUtensorMap* map, const Layout& L, const T* base, int box_rows, int box_cols = M3<T>::RW) {
     auto fn = encode_fn();
     if (!fn) return cudaErrorNotSupported;
     const cuuint64_t dims[3] = {(cuuint64_t)L.px, (cuuint64_t)(L.pp / L.px), (cuuint64_t)(L.alloc / L.pp)};
     const cuuint64_t strides[2] = {(cuuint64_t)L.px * sizeof(T), (cuuint64_t)L.pp * sizeof(T)};
-    const cuuint32_t box[3] = {(cuuint32_t)M3<T>::RW, (cuuint32_t)box_rows, 1};
+    const cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                     const_cast<T*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -409,11 +632,12 @@ static cudaError_t make_map(CUtensorMap* map, const Layout& L, const T* base, in
 
 template <class T, int S, bool FZ, int NM>
 cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
-                                 T omega, const NormOut& no, cudaStream_t s, const Layout* Lc) {
+                                 T omega, const NormOut& no, cudaStream_t s, const Layout* Lc, const T* ec) {
     using G = M3<T>;
+    constexpr size_t smem = M3S<T, NM>::smem;
     {  // per device, so set on every launch (host-side, cheap)
         cudaError_t e = cudaFuncSetAttribute(k_sweep3d_march<T, S, FZ, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)G::smem);
+                                             (int)smem);
         if (e != cudaSuccess) return e;
     }
     // base pointers of the allocations (the layout origin is an offset into them)
@@ -423,9 +647,14 @@ cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo,
     if (e != cudaSuccess) return e;
     e = make_map<T>(&bm, L, b, G::BR);
     if (e != cudaSuccess) return e;
+    CUtensorMap em = bm;  // K3 + K1: the coarse correction tile
+    if (NM == 4) {
+        e = make_map<T>(&em, *Lc, ec, G::ER, G::ECW);
+        if (e != cudaSuccess) return e;
+    }
     static int occ = 0;
     if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep3d_march<T, S, FZ, NM>, M3_THREADS, G::smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep3d_march<T, S, FZ, NM>, M3_THREADS, smem);
         if (occ <= 0) occ = 1;
     }
     const int tx = (L.n + G::TX - 1) / G::TX, ty = (L.n + G::TY - 1) / G::TY;
@@ -435,13 +664,14 @@ cudaError_t launch_sweep3d_march(const Layout& L, const T* x, const T* b, T* xo,
     const int planes = (span + chunks - 1) / chunks;
     chunks = (span + planes - 1) / planes;
     dim3 g(tx, ty, chunks);
-    return launch_k(k_sweep3d_march<T, S, FZ, NM>, g, dim3(M3_THREADS), G::smem, s, L, xm, bm, x, xo, M, sA, sM,
+    return launch_k(k_sweep3d_march<T, S, FZ, NM>, g, dim3(M3_THREADS), smem, s, L, xm, bm, em, x, xo, M, sA, sM,
                       omega, planes, no, Lc ? *Lc : L);
 }
 
 #define SPAIMG_M3_INST(T, S, FZ, NM)                                                                           \
     template cudaError_t launch_sweep3d_march<T, S, FZ, NM>(const Layout&, const T*, const T*, T*, const Terms<T>&, \
-                                                            T, T, T, const NormOut&, cudaStream_t, const Layout*);
+                                                            T, T, T, const NormOut&, cudaStream_t, const Layout*,     \
+                                                            const T*);
 #define SPAIMG_M3_INST4(T, S) \
     SPAIMG_M3_INST(T, S, false, 0) SPAIMG_M3_INST(T, S, true, 0) SPAIMG_M3_INST(T, S, false, 1) SPAIMG_M3_INST(T, S, true, 1)
 SPAIMG_M3_INST4(double, SHAPE_GENERIC)
@@ -454,5 +684,9 @@ SPAIMG_M3_INST(double, SHAPE_C1, false, 2)
 SPAIMG_M3_INST(float, SHAPE_C1, false, 2)
 SPAIMG_M3_INST(double, SHAPE_C1, false, 3)
 SPAIMG_M3_INST(float, SHAPE_C1, false, 3)
+SPAIMG_M3_INST(double, SHAPE_C1, false, 4)
+SPAIMG_M3_INST(float, SHAPE_C1, false, 4)
+SPAIMG_M3_INST(double, SHAPE_STAR7, false, 4)
+SPAIMG_M3_INST(float, SHAPE_STAR7, false, 4)
 
 }  // namespace spaimg

@@ -948,7 +948,7 @@ template <class T> struct Solver final : spaimg_solver {
     Level0Plan make_plan(bool with_a) const {
         const int nu1 = cfg.nu1, nu2 = cfg.nu2;
         const bool two0 = nsmooth() >= 1 && two_ok(0);
-        const bool pc_ok = nsmooth() >= 1 && nu2 >= 1 && fused && sweep_pc_supported(lv[0].L);
+        const bool pc_ok = nsmooth() >= 1 && nu2 >= 1 && fused && sweep_pc_supported(lv[0].L, shape);
         const bool has_a = with_a && fused_norm;
         Level0Plan best;
         int best_pairs = -1;
@@ -1040,7 +1040,7 @@ template <class T> struct Solver final : spaimg_solver {
         // post-smoothing; the prolongation + correction (multigrid.py:184) fused into the first
         // post pass where the level allows it
         int ppairs = l == 0 ? plan0->post_pairs : (two ? 1 << 20 : 0);
-        const bool pc = l == 0 ? plan0->pc : (cfg.nu2 >= 1 && fused && sweep_pc_supported(L.L));
+        const bool pc = l == 0 ? plan0->pc : (cfg.nu2 >= 1 && fused && sweep_pc_supported(L.L, shape));
         int k = 0;
         if (pc) {
             const bool pair = two && ppairs > 0 && cfg.nu2 >= 2;

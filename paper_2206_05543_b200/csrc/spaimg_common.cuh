@@ -201,9 +201,9 @@ __device__ __forceinline__ T fw(T a, T b, T c) {
 template <class T>
 __device__ __forceinline__ T pl_even(T am1, T a0, bool first, bool last) {
     using O = Op<T>;
-    if (first) return O::mul(T(0.5), a0);
-    if (last) return O::mul(T(0.5), am1);
-    return O::mul(T(0.5), O::add(am1, a0));
+    // one multiply for all three cases (the same values bit for bit: only the operand differs)
+    const T s = first ? a0 : (last ? am1 : O::add(am1, a0));
+    return O::mul(T(0.5), s);
 }
 
 }  // namespace spaimg
