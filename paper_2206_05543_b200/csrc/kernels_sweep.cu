@@ -161,6 +161,7 @@ struct M2Ctx {
     const T* erow0;   // coarse row 0 at coarse column c0/2 - VEC
     long long epx;
     int m, ce0;       // coarse interior size, first staged coarse column
+    bool pc_edge;     // the strip (with its halo) holds coarse column 0 or m
 };
 
 __device__ __forceinline__ int fl2(int q) { return q >= 0 ? q / 2 : -((1 - q) / 2); }  // floor(q/2)
@@ -169,7 +170,8 @@ __device__ __forceinline__ int fl2(int q) { return q >= 0 ? q / 2 : -((1 - q) / 
 // index si): separable d-linear interpolation, axis 0 first, with the reference end formulas
 // (multigrid.py:122-144) -- the k_prolong_correct2d tree.  Outside the interior P e is exactly
 // 0 (zero frame), so halo columns/rows stay 0.
-template <class T>
+// EDGE = false: no first/last line of either axis is involved (warp-uniform fast path, no selects).
+template <class T, bool EDGE>
 __device__ __forceinline__ void m2_correct(const M2Ctx<T>& c, T* xrow, int q, int k0, int si) {
     constexpr int VEC = m2_vec<T>();
     const int CRW = c.crw;
@@ -179,15 +181,15 @@ __device__ __forceinline__ void m2_correct(const M2Ctx<T>& c, T* xrow, int q, in
     const int J0 = k0 >> 1;
     T t[VEC / 2 + 1];
     if (q & 1) {
-        const T* e0 = row((q - 1) >> 1);
+        const T* e0 = row((q - 1) >> 1) + J0 - 1;
 #pragma unroll
-        for (int i = 0; i <= VEC / 2; ++i) t[i] = e0[J0 - 1 + i];
+        for (int i = 0; i <= VEC / 2; ++i) t[i] = e0[i];
     } else {
         const int I = q >> 1;
-        const T* em = row(I - 1);
-        const T* e0 = row(I);
+        const T* em = row(I - 1) + J0 - 1;
+        const T* e0 = row(I) + J0 - 1;
 #pragma unroll
-        for (int i = 0; i <= VEC / 2; ++i) t[i] = pl_even<T>(em[J0 - 1 + i], e0[J0 - 1 + i], I == 0, I == c.m);
+        for (int i = 0; i <= VEC / 2; ++i) t[i] = pl_even<T>(em[i], e0[i], EDGE && I == 0, EDGE && I == c.m);
     }
     // axis 1: even column 2J -> pl_even(t(J-1), t(J)), odd column 2J+1 -> t(J)
     T xv[VEC];
@@ -195,24 +197,33 @@ __device__ __forceinline__ void m2_correct(const M2Ctx<T>& c, T* xrow, int q, in
 #pragma unroll
     for (int i = 0; i < VEC / 2; ++i) {
         const int J = J0 + i;
-        xv[2 * i] = O::add(xv[2 * i], pl_even<T>(t[i], t[i + 1], J == 0, J == c.m));
+        xv[2 * i] = O::add(xv[2 * i], pl_even<T>(t[i], t[i + 1], EDGE && J == 0, EDGE && J == c.m));
         xv[2 * i + 1] = O::add(xv[2 * i + 1], t[i + 1]);
     }
     V16<T>::st(xrow + si, xv);
 }
 
-// consumers correct the whole staged x row q (own columns; threads 0/1 also the strip halos)
+// the whole staged x row q: every consumer its own columns, producer lanes 0 / 1 the strip halos
+// (the producer warp is otherwise idle after the barrier, and a consumer warp doing them would
+// run the correction twice)
 template <class T>
 __device__ __forceinline__ void m2_correct_row(const M2Ctx<T>& c, int q, int slot) {
     constexpr int VEC = m2_vec<T>();
     constexpr int W = m2_width<T>();
     constexpr int RW = m2_rowlen<T>();
     T* xrow = c.xs + slot * RW;
-    m2_correct<T>(c, xrow, q, c.col, c.sidx);
-    // the strip halos go to the first and the last consumer (different warps)
-    const int t = c.sidx / VEC - 1;  // consumer thread index 0..(W/VEC - 1)
-    if (t == 0) m2_correct<T>(c, xrow, q, c.c0 - VEC, 0);
-    if (t == W / VEC - 1) m2_correct<T>(c, xrow, q, c.c0 + W, VEC + W);
+    // first/last lines: coarse row 0 / m on even fine rows, coarse column 0 / m inside the strip
+    const bool edge = c.pc_edge || q <= 0 || q >= 2 * c.m;
+    int k0 = c.col, si = c.sidx;
+    if (c.producer) {
+        if (c.lane >= 2) return;
+        k0 = c.lane == 0 ? c.c0 - VEC : c.c0 + W;
+        si = c.lane == 0 ? 0 : VEC + W;
+    }
+    if (edge)
+        m2_correct<T, true>(c, xrow, q, k0, si);
+    else
+        m2_correct<T, false>(c, xrow, q, k0, si);
 }
 
 template <class T, int S, bool FZ, int NM = 0, bool TW = false>
@@ -315,6 +326,13 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
     if (c.producer) {
         // stage j-1 was last read before this barrier: refill its slot with row j-1+ST
         if (c.lane == 0 && j - 1 + ST <= c.q_last) m2_issue<T, S, FZ, NM, TW>(c, j - 1 + ST, sm);
+        if constexpr (NM == 3) {  // the strip halos of row j+3 (see m2_correct_row)
+            constexpr int s3 = (P + 3) % ST;
+            if (j + 3 <= c.q_last) {
+                mbar_wait(&c.full[s3], (uint32_t)(((k + 3) / ST) & 1));
+                m2_correct_row<T>(c, j + 3, s3);
+            }
+        }
         return;
     }
     if (NM == 2) return;
@@ -417,7 +435,7 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
 }
 
 template <class T, int S, bool FZ, int NM, bool TW = false>
-__global__ void __launch_bounds__((M2_NW + 1) * 32, TW ? 3 : 1) k_sweep2d_march(Layout L, const T* __restrict__ x,
+__global__ void __launch_bounds__((M2_NW + 1) * 32, TW ? 3 : (NM == 3 ? 5 : 1)) k_sweep2d_march(Layout L, const T* __restrict__ x,
                                                                      const T* __restrict__ b, T* __restrict__ xo,
                                                                      Terms<T> M, T sA, T sM, T omega, int rows,
                                                                      NormOut no, const T* __restrict__ e, Layout Lc) {
@@ -461,6 +479,7 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32, TW ? 3 : 1) k_sweep2d_march(
         c.erow0 = e + Lc.origin + c.ce0;
         c.epx = Lc.px;
         c.m = Lc.n;
+        c.pc_edge = c.c0 - VEC <= 0 || ((c.c0 + W + VEC) >> 1) >= Lc.n;
     }
 
     if (threadIdx.x == 0) {
@@ -481,11 +500,10 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32, TW ? 3 : 1) k_sweep2d_march(
     mbar_wait(&c.full[0], 0);
     mbar_wait(&c.full[1], 0);
     if constexpr (NM == 3) {  // rows q0 .. q0+3 corrected before the march (then 2 steps ahead)
-        if (!c.producer)
-            for (int i = 0; i < 4 && c.q0 + i <= c.q_last; ++i) {
-                mbar_wait(&c.full[i], 0);
-                m2_correct_row<T>(c, c.q0 + i, i);
-            }
+        for (int i = 0; i < 4 && c.q0 + i <= c.q_last; ++i) {
+            mbar_wait(&c.full[i], 0);
+            m2_correct_row<T>(c, c.q0 + i, i);
+        }
         __syncthreads();
     }
     if (!FZ && !c.producer) {
