@@ -8,8 +8,8 @@
 // x(j-1..j+1) and r(j-2..j) of them in registers (register-blocked z-marching); r(j) of the
 // tile plus its one-point ring goes to a 3-plane shared ring from which M takes its in-plane
 // neighbours.  r is computed once per tile point (the ring is recomputed by the neighbour
-// tile: 2(TX+TY)/(TX*TY) extra).  The step loop is unrolled by 12 = lcm(4 stages, 3 rows) so
-// every ring index is a compile-time constant.
+// tile: 2(TX+TY)/(TX*TY) extra).  The step loop is unrolled by 3 so the register-array and
+// r-ring indices are compile-time constants; the stage slots (k mod 4) are runtime.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -313,8 +313,12 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
     static_assert(!PC || (S != SHAPE_GENERIC && !FZ), "K3 + K1: named shapes, a given iterate");
     constexpr int VEC = G::VEC;
     constexpr int RW = G::RW;
-    constexpr int sj = P % M3_ST, sp = (P + 1) % M3_ST, sm = (P + M3_ST - 1) % M3_ST;
-    constexpr int bj_slot = PC ? (P + 2) % 3 : P % M3_ST;  // b(j): K3 + K1 stages b(q0 + 1 + i) in slot i % 3
+    // P = k mod 3 fixes the register-array and r / b ring indices at compile time; the x stage
+    // slots are runtime (k mod 4), which keeps the unrolled march at 3 steps (a 12-step unroll
+    // made every ring index a constant but overflowed the instruction cache in the larger variants)
+    static_assert(M3_ST == 4, "stage slots are k & 3");
+    const int sj = k & 3, sp = (k + 1) & 3, sm = (k + 3) & 3, s2 = (k + 2) & 3;
+    const int bj_slot = PC ? (P + 2) % 3 : sj;  // b(j): K3 + K1 stages b(q0 + 1 + i) in slot i % 3
     constexpr int ic = P % 3, ip = (P + 1) % 3, im = (P + 2) % 3;
     // r ring: planes j, j-1, j-2 (the two-plane ring of the K3 + K1 variant never reads r(j-2))
     constexpr int rj = P % SP::RRD, rj1 = (P + SP::RRD - 1) % SP::RRD, rj2 = (P + 1) % SP::RRD;
@@ -324,7 +328,7 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
     if constexpr (S == SHAPE_GENERIC || NM == 3) __syncthreads();
     if constexpr (PC) {
         // plane j+1 arrived (and was corrected) a step ago; plane j+2 is corrected in this step
-        if (j + 2 <= c.q_last) mbar_wait(&c.full[(P + 2) % M3_ST], (uint32_t)(((k + 2) / M3_ST) & 1));
+        if (j + 2 <= c.q_last) mbar_wait(&c.full[s2], (uint32_t)(((k + 2) / M3_ST) & 1));
     } else {
         mbar_wait(&c.full[sp], (uint32_t)(((k + 1) / M3_ST) & 1));
     }
@@ -388,7 +392,7 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
     if constexpr (PC) {
         // x + P e on the staged plane j+2 (tile and halo), in place, a step before anything reads
         // it: independent of the r(j) work above, ordered before the next step by the barrier below
-        if (j + 2 <= c.q_last) m3_correct_plane<T>(c, j + 2, (P + 2) % M3_ST, ecs);
+        if (j + 2 <= c.q_last) m3_correct_plane<T>(c, j + 2, s2, ecs);
         // ecs follows floor(q/2) mod EST of the plane corrected next
         if (j & 1) ecs = ecs == G::EST - 1 ? 0 : ecs + 1;
     }
@@ -426,7 +430,7 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
             T acc = T(0);
             if constexpr (S == SHAPE_GENERIC) {
                 // runtime term list: every r value (own points included) is in the shared r ring,
-                // so a rolled loop keeps the 12-step unrolled body small
+                // so a rolled loop keeps the unrolled body small
 #pragma unroll 1
                 for (int t = 0; t < nt; ++t) {
                     const int o0 = M.off[t][0];
@@ -589,12 +593,11 @@ __global__ void __launch_bounds__(M3_THREADS, 2)
     double nacc = 0.0;
     int ecs = SP::PC ? G::eslot((c.q0 + 3) >> 1) : 0;  // step k = 1 corrects plane q0 + 3
     const int K = z_end - c.q0;  // steps k = 1..K (planes j = z0-1 .. z_end)
-    for (int kb = 0; kb <= K; kb += 12) {
+    for (int kb = 0; kb <= K; kb += 3) {
 #define M3STEP(p)                                                                            \
     if (kb + (p) >= 1 && kb + (p) <= K)                                                     \
         m3_step<T, S, FZ, NM, (p)>(c, &xmap, &bmap, &emap, kb + (p), X, R, XP, ecs, M, sA, sM, omega, nacc);
-        M3STEP(0) M3STEP(1) M3STEP(2) M3STEP(3) M3STEP(4) M3STEP(5)
-        M3STEP(6) M3STEP(7) M3STEP(8) M3STEP(9) M3STEP(10) M3STEP(11)
+        M3STEP(0) M3STEP(1) M3STEP(2)
 #undef M3STEP
     }
     if (NM == 1 || NM == 2) norm_epilogue(nacc, no);

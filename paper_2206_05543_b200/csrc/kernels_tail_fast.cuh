@@ -16,6 +16,8 @@
 // follows the last op of a visit of l+1.  One named barrier id per warp count.
 #pragma once
 
+#include <climits>
+
 #include "tail_ops.cuh"
 
 namespace spaimg {
@@ -191,9 +193,61 @@ struct FastTail {
         }
     }
 
+    // entry level in: b (and the start iterate unless the entry is from zero) of the box
+    // [-1, n+1)^D of the global padded layout, whose frame is zero.  Compile-time geometry: the
+    // loop is unrolled in batches of 8 points whose global loads are all issued before the first
+    // store (a rolled loop waited out one L2 round trip per iteration).
+    __device__ static __forceinline__ void load_entry(const TailArgs<T>& a, T* arr, bool fz) {
+        constexpr int W0 = w(0), CNT = D == 2 ? W0 * W0 : W0 * W0 * W0;
+        constexpr int IT = (CNT + NT - 1) / NT, UB = 8;
+        const long long p0 = D == 2 ? a.gL.px : a.gL.pp;
+#pragma unroll 1
+        for (int ib = 0; ib < IT; ib += UB) {
+            T vb[UB], vx[UB];
+            int so[UB];
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const int qq = (ib + u) * NT + (int)threadIdx.x;
+                so[u] = INT_MIN;
+                vb[u] = vx[u] = T(0);
+                if (ib + u < IT && qq < CNT) {
+                    const int j0 = (D == 2 ? qq / W0 : qq / (W0 * W0)) - 1;
+                    const int rem = D == 2 ? 0 : qq % (W0 * W0);
+                    const int j1 = D == 2 ? 0 : rem / W0 - 1;
+                    const int j2 = (D == 2 ? qq % W0 : rem % W0) - 1;
+                    const long long g = a.gL.origin + (long long)j0 * p0 + (D == 3 ? (long long)j1 * a.gL.px : 0LL) + j2;
+                    so[u] = j0 * s0(0) + j1 * s1(0) + j2;
+                    vb[u] = a.gb[g];
+                    if (!fz) vx[u] = a.gx[g];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UB; ++u)
+                if (so[u] != INT_MIN) {
+                    arr[bo(0) + so[u]] = vb[u];
+                    arr[xo(0) + so[u]] = vx[u];
+                }
+        }
+    }
+
+    // entry level out: the iterate's interior back to the global padded layout
+    __device__ static __forceinline__ void store_entry(const TailArgs<T>& a, const T* arr) {
+        constexpr int N0 = n(0), CNT = D == 2 ? N0 * N0 : N0 * N0 * N0;
+        const long long p0 = D == 2 ? a.gL.px : a.gL.pp;
+#pragma unroll 4
+        for (int qq = threadIdx.x; qq < CNT; qq += NT) {
+            const int j0 = D == 2 ? qq / N0 : qq / (N0 * N0);
+            const int rem = D == 2 ? 0 : qq % (N0 * N0);
+            const int j1 = D == 2 ? 0 : rem / N0;
+            const int j2 = D == 2 ? qq % N0 : rem % N0;
+            a.gx[a.gL.origin + (long long)j0 * p0 + (D == 3 ? (long long)j1 * a.gL.px : 0LL) + j2] =
+                arr[xo(0) + j0 * s0(0) + j1 * s1(0) + j2];
+        }
+    }
+
     __device__ static __forceinline__ void run(const TailArgs<T>& a, T* arr) {
         const int t = threadIdx.x;
-        tail_load_entry<T, D>(a, arr, xo(0), bo(0), s0(0), s1(0));
+        load_entry(a, arr, a.entry_fz != 0);
         for (int i = zero_from() + t; i < elems(); i += NT) arr[i] = T(0);
         if constexpr (kDebugChecks) {
             __syncthreads();
@@ -224,7 +278,7 @@ struct FastTail {
         visit<0>(a, arr, t >> 5, pc, a.entry_fz != 0, false, false);
         __syncthreads();
         if (a.prof && t == 0) a.prof[pc] = clock64();
-        tail_store_entry<T, D>(a, arr, xo(0), s0(0), s1(0));
+        store_entry(a, arr);
     }
 };
 
