@@ -254,9 +254,9 @@ __device__ __forceinline__ void m3_correct_plane(const M3Ctx<T>& c, int q, int s
     fence_proxy_async_smem();  // the slot is refilled by TMA later
 }
 
-// r at a tile-local ring point (ry, rx) of plane j, all operands from shared memory.  CACHE (K3 +
-// K1): x(j-1) at the point comes from `prev` (this thread read it as x(j) a step ago), so x(j-1)'s
-// stage is not touched; prev is then advanced to x(j).
+// r at this thread's ring point (stage offset ro) of plane j.  CACHE (every mode that stages x):
+// x(j-1) at the point comes from `prev` (this thread read it as x(j) a step ago), so x(j-1)'s
+// stage is not touched and can be refilled a step earlier; prev is then advanced to x(j).
 template <class T, bool FZ, bool CACHE>
 __device__ __forceinline__ T m3_ring_r(const M3Ctx<T>& c, int sj, int sp, int sm, int sb, int ro, bool in, int j, T sA,
                                        T& prev) {
@@ -386,7 +386,7 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
 #pragma unroll
         for (int i = 0; i < G::NRP; ++i) {
             if (c.rro[i] >= 0)
-                rpl[c.rro[i]] = m3_ring_r<T, FZ, PC>(c, sj, sp, sm, bj_slot, c.rro[i], c.rin[i], j, sA, XP[i]);
+                rpl[c.rro[i]] = m3_ring_r<T, FZ, !FZ>(c, sj, sp, sm, bj_slot, c.rro[i], c.rin[i], j, sA, XP[i]);
         }
     }
     if constexpr (PC) {
@@ -397,11 +397,10 @@ __device__ __forceinline__ void m3_step(const M3Ctx<T>& c, const CUtensorMap* xm
         if (j & 1) ecs = ecs == G::EST - 1 ? 0 : ecs + 1;
     }
     __syncthreads();
-    if constexpr (PC) {  // x(j) is dead from here on (see M3S): its stage takes x(j+4)
-        if (c.tid == 0 && j + M3_ST <= c.q_last) m3_issue<T, FZ, NM>(c, xmap, bmap, emap, j + M3_ST, sj);
-    } else {
-        if (c.tid == 0 && j - 1 + M3_ST <= c.q_last) m3_issue<T, FZ, NM>(c, xmap, bmap, emap, j - 1 + M3_ST, sm);
-    }
+    // x(j)'s stage is dead from here on: the step's own reads are done, the ring points' x(j-1)
+    // of the next step comes from registers (XP), and the output phase reads r planes and
+    // registers only.  It takes plane j+4 (three steps of lead; K3 + K1: two, see M3S).
+    if (c.tid == 0 && j + M3_ST <= c.q_last) m3_issue<T, FZ, NM>(c, xmap, bmap, emap, j + M3_ST, sj);
     if constexpr (NM == 3) {
         if ((j & 1) == 0 && j >= c.z0 + 1)
             m3_restrict_out<T>(c, j, c.rr + rj * G::RS, c.rr + rj1 * G::RS, c.rr + rj2 * G::RS, R[ic], R[im], R[ip]);
@@ -574,22 +573,22 @@ __global__ void __launch_bounds__(M3_THREADS, 2)
         mbar_wait(&c.full[2], 0);
         m3_correct_plane<T>(c, c.q0 + 2, 2, G::eslot((c.q0 + 2) >> 1));
         __syncthreads();
+    }
+    if (!FZ) {
         // x(q0) at this thread's ring point(s): x(j-1) of the first step
 #pragma unroll
         for (int i = 0; i < G::NRP; ++i)
             if (c.rro[i] >= 0) XP[i] = c.xs[G::RW + c.rro[i]];
-    }
-    if (!FZ) {
 #pragma unroll
         for (int yy = 0; yy < 2; ++yy) {
             V16<T>::ld(c.xs + 0 * G::XS + (c.yl + yy + 2) * G::RW + VEC + c.xl, X[0][yy]);
             V16<T>::ld(c.xs + 1 * G::XS + (c.yl + yy + 2) * G::RW + VEC + c.xl, X[1][yy]);
         }
     }
-    if constexpr (SP::PC) {  // every read of x(q0)'s stage is done: it takes x(q0 + 4)
-        __syncthreads();
-        if (threadIdx.x == 0 && c.q0 + M3_ST <= c.q_last) m3_issue<T, FZ, NM>(c, &xmap, &bmap, &emap, c.q0 + M3_ST, 0);
-    }
+    // every read of plane q0's stage is done (no step reads it: x(q0) lives in registers, b(q0) is
+    // unused): it takes plane q0 + 4
+    __syncthreads();
+    if (threadIdx.x == 0 && c.q0 + M3_ST <= c.q_last) m3_issue<T, FZ, NM>(c, &xmap, &bmap, &emap, c.q0 + M3_ST, 0);
     double nacc = 0.0;
     int ecs = SP::PC ? G::eslot((c.q0 + 3) >> 1) : 0;  // step k = 1 corrects plane q0 + 3
     const int K = z_end - c.q0;  // steps k = 1..K (planes j = z0-1 .. z_end)
