@@ -229,8 +229,8 @@ __device__ __forceinline__ void m3_halo_block(int h, int& ry, int& rx) {
 }
 
 // the whole staged x plane q in `slot`, in place: every thread its own 2 x VEC block, the first
-// NHALO threads also one block of the halo frame (a rolled two-pass loop keeps the unrolled march
-// small; the blocks' stage offsets are per-thread constants, M3Ctx::pxo / peo)
+// NHALO threads also one block of the halo frame (the blocks' stage offsets are per-thread
+// constants, M3Ctx::pxo / peo)
 // es0: the ring slot of coarse plane floor(q/2) (the plane an odd q copies, the upper plane of an
 // even q); the plane below is one slot back
 template <class T>
@@ -241,15 +241,13 @@ __device__ __forceinline__ void m3_correct_plane(const M3Ctx<T>& c, int q, int s
     const bool edge = c.pc_edge || q <= 0 || q >= 2 * c.cm;
     const T* e0 = c.es + es0 * G::ES;
     const T* em = c.es + (es0 == 0 ? G::EST - 1 : es0 - 1) * G::ES;
-#pragma unroll 1
-    for (int pass = 0; pass < 2; ++pass) {
-        if (pass && c.tid >= G::NHALO) break;
-        // (selects, not indexing: a runtime index would put the context in local memory)
-        const int xo = pass ? c.pxo[1] : c.pxo[0], eo = pass ? c.peo[1] : c.peo[0];
-        if (edge)
-            m3_correct<T, true>(c, xpl + xo, em + eo, e0 + eo, q, pass ? c.pry[1] : c.pry[0], pass ? c.prx[1] : c.prx[0]);
-        else
-            m3_correct<T, false>(c, xpl + xo, em + eo, e0 + eo, q, 0, 0);
+    const bool halo = c.tid < G::NHALO;
+    if (edge) {
+        m3_correct<T, true>(c, xpl + c.pxo[0], em + c.peo[0], e0 + c.peo[0], q, c.pry[0], c.prx[0]);
+        if (halo) m3_correct<T, true>(c, xpl + c.pxo[1], em + c.peo[1], e0 + c.peo[1], q, c.pry[1], c.prx[1]);
+    } else {
+        m3_correct<T, false>(c, xpl + c.pxo[0], em + c.peo[0], e0 + c.peo[0], q, 0, 0);
+        if (halo) m3_correct<T, false>(c, xpl + c.pxo[1], em + c.peo[1], e0 + c.peo[1], q, 0, 0);
     }
     fence_proxy_async_smem();  // the slot is refilled by TMA later
 }
