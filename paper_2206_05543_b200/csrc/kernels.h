@@ -119,7 +119,6 @@ enum TailOpType : int {
     TAIL_COARSE = 6,   // x = (LU)^-1 b in getrs order                (multigrid.py:147-154)
     // fused ops of the compile-time engine (kernels_tail_fast.cuh; host-side labels only)
     TAIL_RESFW = 7,        // RES + FW
-    TAIL_PROLONG_RES = 8,  // PROLONG + the next RES
 };
 // One op = one packed word (host-recorded): type | level << 3 | nw << 6 | bw << 11 | bid << 16
 //   level: index into TailArgs::lv (0 = the entry level); FW / PROLONG also use level + 1

@@ -108,34 +108,30 @@ struct FastTail {
         ++pc;
     }
 
-    // fused small-level ops (tail_ops.cuh): residual + restriction where the coarse box maps one
-    // point per thread (3D: fine n <= 7, whose 27-point footprint stays cheap), prolongation +
-    // the next residual where the fine box does
+    // residual + restriction in one op (tail_ops.cuh op_resfw) where the coarse box maps one point
+    // per thread, 2D only.  Measured per op with SPAIMG_TAIL_PROF and per cycle with
+    // tools/tail_variants.sh: in 3D the 27-point footprint costs more than the barrier it saves
+    // (n = 7: 1656 cycles fused, ~850 as residual, barrier, restriction; c3 V(1,1) 117 -> 114
+    // us/cycle unfused); in 2D it is neutral.  A fused prolongation + next residual (every thread
+    // interpolating the correction at its point and its 2 D neighbours) was removed: it cost 1100
+    // cycles against ~730 unfused at n = 15 in 2D and 6600 against ~2100 at n = 7 in 3D; without
+    // it c2 W(1,0) went 2.46 -> 2.28 ms/cycle, c2 V(1,1) 0.379 -> 0.373, c3 V(1,1) 127 -> 117 us.
     __host__ __device__ static constexpr bool fuse_rr(int l) {
-        return l + 1 < NL && (1 << (D * (LE - l - 1))) <= NTH(l + 1) && (D == 2 || LE - l <= 3);
+        return D == 2 && l + 1 < NL && (1 << (D * (LE - l - 1))) <= NTH(l + 1);
     }
-    __host__ __device__ static constexpr bool fuse_pr(int l) { return l + 1 < NL && (1 << (D * (LE - l))) <= NTH(l); }
 
-    // visit of level L (multigrid.py:157-185).  fz: from a zero iterate; res_done: the residual of
-    // the start iterate is already in r (the previous op was a fused prolongation + residual);
-    // res_next: the op after this visit is the residual of the next visit of this level (nu1 >= 1),
-    // so the closing prolongation may form it.
+    // visit of level L (multigrid.py:157-185); fz: from a zero iterate
     template <int L>
-    __device__ static __forceinline__ void visit(const TailArgs<T>& a, T* arr, int warp, int& pc, bool fz,
-                                                 bool res_done, bool res_next) {
+    __device__ static __forceinline__ void visit(const TailArgs<T>& a, T* arr, int warp, int& pc, bool fz) {
         constexpr int PL = P(L), PC = PF(L), LW = logw(L), TL = NTH(L), TC = NTH(L + 1);
         const TailLv<T> f = geo(a, L);
         const TailLv<T> c = geo(a, L + 1);
         for (int k = 0; k < a.nu1; ++k) {
             if (fz && k == 0) {
-                step<PL, PL>(a, warp, pc, [&] { op_relax<T, S, D, LW, true, false, TL>(f, arr, a.M, a.omega); });
-            } else if (res_done && k == 0) {
-                // the previous visit closed with a fused prolongation + residual: apply its correction here
-                if constexpr (fuse_pr(L))
-                    step<PL, PL>(a, warp, pc, [&] { op_relax<T, S, D, LW, false, true, TL>(f, arr, a.M, a.omega, &c); });
+                step<PL, PL>(a, warp, pc, [&] { op_relax<T, S, D, LW, true, TL>(f, arr, a.M, a.omega); });
             } else {
                 step<PL, PL>(a, warp, pc, [&] { op_res<T, D, LW, TL>(f, arr); });
-                step<PL, PL>(a, warp, pc, [&] { op_relax<T, S, D, LW, false, false, TL>(f, arr, a.M, a.omega); });
+                step<PL, PL>(a, warp, pc, [&] { op_relax<T, S, D, LW, false, TL>(f, arr, a.M, a.omega); });
             }
         }
         if (fz && a.nu1 == 0) step<PL, PL>(a, warp, pc, [&] { op_zero<T, D, LW, TL>(f, arr); });
@@ -154,42 +150,20 @@ struct FastTail {
                 if (threadIdx.x == 0) coarse_fast<T, NLU>(cf, ci, arr + bo(L + 1), arr + xo(L + 1));
             });
         } else {
-            // a visit of L+1 that ends with its prolongation (nu2 == 0) and is followed by another
-            // one starting with a residual (nu1 >= 1) hands that residual over
-            const bool sib = fuse_pr(L + 1) && a.nu1 >= 1 && a.nu2 == 0;
-            for (int g = 0; g < a.gamma; ++g)
-                visit<L + 1>(a, arr, warp, pc, g == 0, sib && g > 0, sib && g + 1 < a.gamma);
+            for (int g = 0; g < a.gamma; ++g) visit<L + 1>(a, arr, warp, pc, g == 0);
         }
-        // prolongation + correction (multigrid.py:184), with the next sweep's residual when one follows
+        // prolongation + correction (multigrid.py:184)
 #ifdef SPAIMG_DEBUG_BREAK_BARRIER
         // fault injection for the checked-build self-test (tools/README): no barrier before the
         // prolongation, so it may read the coarse correction before the coarse visit wrote it
-        if constexpr (!fuse_pr(L)) {
-            if (warp < PL) {
-                ++pc;
-                op_prolong<T, D, LW, TL>(f, c, arr);
-            } else {
-                ++pc;
-            }
-        } else
+        if (warp < PL) op_prolong<T, D, LW, TL>(f, c, arr);
+        ++pc;
+#else
+        step<PL, PL>(a, warp, pc, [&] { op_prolong<T, D, LW, TL>(f, c, arr); });
 #endif
-        if constexpr (fuse_pr(L)) {
-            if (a.nu2 >= 1 || res_next)
-                step<PL, PL>(a, warp, pc, [&] { op_prolong_res<T, D, LW, TL>(f, c, arr); });
-            else
-                step<PL, PL>(a, warp, pc, [&] { op_prolong<T, D, LW, TL>(f, c, arr); });
-        } else {
-            step<PL, PL>(a, warp, pc, [&] { op_prolong<T, D, LW, TL>(f, c, arr); });
-        }
         for (int k = 0; k < a.nu2; ++k) {
-            if constexpr (fuse_pr(L)) {
-                if (k == 0) {
-                    step<PL, PL>(a, warp, pc, [&] { op_relax<T, S, D, LW, false, true, TL>(f, arr, a.M, a.omega, &c); });
-                    continue;
-                }
-            }
             step<PL, PL>(a, warp, pc, [&] { op_res<T, D, LW, TL>(f, arr); });
-            step<PL, PL>(a, warp, pc, [&] { op_relax<T, S, D, LW, false, false, TL>(f, arr, a.M, a.omega); });
+            step<PL, PL>(a, warp, pc, [&] { op_relax<T, S, D, LW, false, TL>(f, arr, a.M, a.omega); });
         }
     }
 
@@ -275,7 +249,7 @@ struct FastTail {
         }
         __syncthreads();
         int pc = 0;
-        visit<0>(a, arr, t >> 5, pc, a.entry_fz != 0, false, false);
+        visit<0>(a, arr, t >> 5, pc, a.entry_fz != 0);
         __syncthreads();
         if (a.prof && t == 0) a.prof[pc] = clock64();
         store_entry(a, arr);

@@ -688,18 +688,13 @@ template <class T> struct Solver final : spaimg_solver {
     bool fast_fuse_rr(int i) const {
         const int lw = tg[i].logw;
         if (i + 1 >= (int)tg.size()) return false;
-        return (1LL << (cfg.dim * (lw - 1))) <= fast_nth(i + 1) && (cfg.dim == 2 || lw <= 3);
+        return cfg.dim == 2 && (1LL << (cfg.dim * (lw - 1))) <= fast_nth(i + 1);
     }
-    bool fast_fuse_pr(int i) const {
-        return i + 1 < (int)tg.size() && (1LL << (cfg.dim * tg[i].logw)) <= fast_nth(i);
-    }
-    void record_fast(int i, bool fz, bool res_done, bool res_next, std::vector<HOp>& ops) const {
+    void record_fast(int i, bool fz, std::vector<HOp>& ops) const {
         const int last = (int)tg.size() - 1;
         for (int k = 0; k < cfg.nu1; ++k) {
             if (fz && k == 0) {
                 ops.push_back(point_op(TAIL_RELAX0, i));
-            } else if (res_done && k == 0) {
-                ops.push_back(point_op(TAIL_RELAX, i));
             } else {
                 ops.push_back(point_op(TAIL_RES, i));
                 ops.push_back(point_op(TAIL_RELAX, i));
@@ -717,14 +712,11 @@ template <class T> struct Solver final : spaimg_solver {
         if (i + 1 == last) {
             ops.push_back(HOp{TAIL_COARSE, last, 1, 0, 0});
         } else {
-            const bool sib = fast_fuse_pr(i + 1) && cfg.nu1 >= 1 && cfg.nu2 == 0;
-            for (int g = 0; g < cfg.gamma; ++g) record_fast(i + 1, g == 0, sib && g > 0, sib && g + 1 < cfg.gamma, ops);
+            for (int g = 0; g < cfg.gamma; ++g) record_fast(i + 1, g == 0, ops);
         }
-        HOp o = point_op(TAIL_PROLONG, i);
-        if (fast_fuse_pr(i) && (cfg.nu2 >= 1 || res_next)) o.type = TAIL_PROLONG_RES;
-        ops.push_back(o);
+        ops.push_back(point_op(TAIL_PROLONG, i));
         for (int k = 0; k < cfg.nu2; ++k) {
-            if (!(k == 0 && fast_fuse_pr(i))) ops.push_back(point_op(TAIL_RES, i));
+            ops.push_back(point_op(TAIL_RES, i));
             ops.push_back(point_op(TAIL_RELAX, i));
         }
     }
@@ -873,7 +865,7 @@ template <class T> struct Solver final : spaimg_solver {
         if (fast)
             for (int fz = 0; fz < 2; ++fz) {
                 prof_ops[fz].clear();
-                record_fast(0, fz != 0, false, false, prof_ops[fz]);
+                record_fast(0, fz != 0, prof_ops[fz]);
             }
         return 0;
     }
@@ -888,8 +880,8 @@ template <class T> struct Solver final : spaimg_solver {
         if (cudaDeviceSynchronize() != cudaSuccess) return;
         cudaMemcpy(c.data(), tail_args[0].prof, c.size() * sizeof(long long), cudaMemcpyDeviceToHost);
         c[ops.size()] = c[ops.size()];
-        static const char* names[] = {"RES", "RELAX", "RELAX0", "ZERO", "FW", "PROLONG", "COARSE", "RESFW", "PRORES"};
-        long long tot[9] = {}, cnt[9] = {};
+        static const char* names[] = {"RES", "RELAX", "RELAX0", "ZERO", "FW", "PROLONG", "COARSE", "RESFW"};
+        long long tot[8] = {}, cnt[8] = {};
         for (size_t i = 0; i < ops.size(); ++i) {
             const long long d = c[i + 1] - c[i];
             tot[ops[i].type] += d;
@@ -900,7 +892,7 @@ template <class T> struct Solver final : spaimg_solver {
             fprintf(stderr, "tailprof op %3zu %-7s n=%2d nw=%2d bw=%2d  %6lld cycles (dispatch %lld body %lld)\n", i,
                     names[ops[i].type], tg[ops[i].level].n, ops[i].nw, ops[i].bw, d, pre, body);
         }
-        for (int k = 0; k < 9; ++k)
+        for (int k = 0; k < 8; ++k)
             if (cnt[k]) fprintf(stderr, "tailprof sum %-7s %3lld ops %8lld cycles\n", names[k], cnt[k], tot[k]);
         fprintf(stderr, "tailprof total %lld cycles\n", c[ops.size()] - c[0]);
     }

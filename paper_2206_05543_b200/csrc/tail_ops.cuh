@@ -140,14 +140,8 @@ __device__ __forceinline__ void op_res(const TailLv<T>& f, T* arr) {
 }
 
 // x = (FROM_ZERO ? 0 : x) + omega ((M src) sM) with src = r (RELAX) or b (RELAX0: r == b)
-template <class T, int D>
-__device__ __forceinline__ T pe_at(const T* e, int m, int cs0, int cs1, int i0, int i1, int i2);
-
-// PEND: x still lacks the prolongated correction of the coarse level `c` (op_prolong_res ran
-// before): x + P e is formed at the point first (multigrid.py:184), then relaxed
-template <class T, int S, int D, int LOGW, bool FROM_ZERO, bool PEND = false, int NTH = NT>
-__device__ __forceinline__ void op_relax(const TailLv<T>& f, T* arr, const Terms<T>& M, T omega,
-                                         const TailLv<T>* c = nullptr) {
+template <class T, int S, int D, int LOGW, bool FROM_ZERO, int NTH = NT>
+__device__ __forceinline__ void op_relax(const TailLv<T>& f, T* arr, const Terms<T>& M, T omega) {
     using O = Op<T>;
     using Q = Strip<D, LOGW, NTH>;
     const Q q(f.n);
@@ -161,10 +155,6 @@ __device__ __forceinline__ void op_relax(const TailLv<T>& f, T* arr, const Terms
     if constexpr (!FROM_ZERO) {
 #pragma unroll
         for (int j = 0; j < K; ++j) xv[j] = x[p0 + j * s0];
-    }
-    if constexpr (PEND) {
-        static_assert(K == 1 && !FROM_ZERO, "pending prolongation: one point per thread");
-        xv[0] = O::add(xv[0], pe_at<T, D>(arr + c->x, c->n, c->s0, c->s1, q.i0, q.i1, q.i2));
     }
     if constexpr (S == SHAPE_GENERIC) {
         T acc[K];
@@ -369,58 +359,6 @@ __device__ __forceinline__ void op_resfw(const TailLv<T>& f, const TailLv<T>& c,
         v = fw<T>(u[0], u[1], u[2]);
     }
     arr[c.b + q.i0 * c.s0 + q.i1 * c.s1 + q.i2] = v;
-}
-
-// (P e) at fine interior point (i0, i1, i2), separable, axis 0 first; coarse values around it
-template <class T, int D>
-__device__ __forceinline__ T pe_at(const T* e, int m, int cs0, int cs1, int i0, int i1, int i2) {
-    const int j0 = i0 >> 1, j1 = i1 >> 1, j2 = i2 >> 1;
-    auto g = [&](int a, int b, int cc) { return e[(j0 - 1 + a) * cs0 + (D == 3 ? (j1 - 1 + b) * cs1 : 0) + (j2 - 1 + cc)]; };
-    T v[2];
-#pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
-        if constexpr (D == 3) {
-            const T u0 = lin<T>(i0, m, g(0, 0, cc), g(1, 0, cc));
-            const T u1 = lin<T>(i0, m, g(0, 1, cc), g(1, 1, cc));
-            v[cc] = lin<T>(i1, m, u0, u1);
-        } else {
-            v[cc] = lin<T>(i0, m, g(0, 0, cc), g(1, 0, cc));
-        }
-    }
-    return lin<T>(i2, m, v[0], v[1]);
-}
-
-// r = b - A (x + P e) in one op: the corrected iterate is formed at the point and at its
-// Laplacian neighbours (zero outside the interior, as the stored frame), so the residual needs no
-// barrier after the prolongation (multigrid.py:184 then :99 of the next sweep).  x itself is NOT
-// updated here (neighbouring threads read it); the relaxation that follows applies the pending
-// correction at its own point (op_relax PEND).  K = 1 boxes only.
-template <class T, int D, int LOGW, int NTH = NT>
-__device__ __forceinline__ void op_prolong_res(const TailLv<T>& f, const TailLv<T>& c, T* arr) {
-    using O = Op<T>;
-    using Q = Strip<D, LOGW, NTH>;
-    static_assert(Q::K == 1, "op_prolong_res maps one point per thread");
-    const Q q(f.n);
-    if (!q.ok) return;
-    const int n = f.n, s0 = f.s0, s1 = f.s1;
-    const int p = q.at(s0, s1);
-    T* x = arr + f.x;
-    const T* e = arr + c.x;
-    const int m = c.n, cs0 = c.s0, cs1 = c.s1;
-    auto xc = [&](int d0, int d1, int d2) {
-        const int i0 = q.i0 + d0, i1 = q.i1 + d1, i2 = q.i2 + d2;
-        const bool in = i0 >= 0 && i0 < n && i2 >= 0 && i2 < n && (D == 2 || (i1 >= 0 && i1 < n));
-        const T v = O::add(x[p + d0 * s0 + d1 * s1 + d2], pe_at<T, D>(e, m, cs0, cs1, i0, i1, i2));
-        return in ? v : T(0);
-    };
-    const T v0 = xc(0, 0, 0);
-    T rv;
-    if constexpr (D == 2)
-        rv = residual2d<T>(arr[f.b + p], v0, xc(1, 0, 0), xc(-1, 0, 0), xc(0, 0, 1), xc(0, 0, -1), f.sA);
-    else
-        rv = residual3d<T>(arr[f.b + p], v0, xc(1, 0, 0), xc(-1, 0, 0), xc(0, 1, 0), xc(0, -1, 0), xc(0, 0, 1),
-                           xc(0, 0, -1), f.sA);
-    arr[f.r + p] = rv;
 }
 
 // ------------------------------------------------------------------------------------------
