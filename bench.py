@@ -303,6 +303,8 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": k1_bytes, "avg_launch_ms": t_k1 * 1e3,
                 "frac_of_8TBs": achieved / 8000.0}
     vcycle_gbs = stats["bytes_per_cycle"] / t_cycle / 1e9
+    _dim, _N, _ = __import__("paper_2206_05543_b200.workloads", fromlist=["CONFIGS"]).CONFIGS[HEADLINE["cfg_id"]]
+    fused_b = fused_bytes_per_cycle(_dim, _N, esz, HEADLINE["nu1"], HEADLINE["nu2"], 1, 2, stats["bytes_per_cycle"])
 
     # ---------------- e2e: public API with pinned host buffers -------------------------------
     # Solver.solve_batch: every step copies its right-hand side in from pinned host memory and
@@ -349,6 +351,8 @@ def run_ours(args):
             "cycles_per_solve": cycles_per_step, "time_to_tol_ms": ms_per_step, "ms_per_cycle": t_cycle * 1e3,
             "bytes_per_cycle": stats["bytes_per_cycle"], "vcycle_gbs": vcycle_gbs,
             "vcycle_roofline_frac": vcycle_gbs / peak, "kernels_per_cycle": stats["kernels_per_cycle"],
+            "fused_bytes_per_cycle": fused_b,
+            "vcycle_fused_roofline_frac": fused_b / t_cycle / 1e9 / peak,
             "converged": all(c for _, c, _ in hists), "final_rel_residual": hists[-1][2],
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -426,6 +430,8 @@ def run_extras(sp, torch, stream, peak):
         out["c4_m7_V11"] = {"cycles": k, "converged": conv, "time_to_tol_ms": t * 1e3, "ms_per_cycle": t / k * 1e3,
                             "dof_per_s": n0 * k / t, "bytes_per_cycle": st["bytes_per_cycle"],
                             "vcycle_roofline_frac": st["bytes_per_cycle"] / (t / k) / 1e9 / peak,
+                            "vcycle_fused_roofline_frac":
+                                fused_bytes_per_cycle(3, N, 8, 1, 1, 1, 2, st["bytes_per_cycle"]) / (t / k) / 1e9 / peak,
                             "sweep_gbs": 24 * n0 / tk / 1e9, "sweep_frac": 24 * n0 / tk / 1e9 / peak,
                             "kernels_per_cycle": st["kernels_per_cycle"]}
         del s3
@@ -485,7 +491,9 @@ def config_sweep(sp, torch, stream, peak):
                 "cycles": k, "converged": conv, "time_to_tol_ms": t * 1e3, "ms_per_cycle": t / k * 1e3,
                 "dof_per_s": (N - 1) ** dim * k / t, "rho_hat": rho,
                 "last_cycle_factor": hist[-1] / hist[-2] if k >= 1 else None,
-                "vcycle_roofline_frac": st["bytes_per_cycle"] / (t / k) / 1e9 / peak}
+                "vcycle_roofline_frac": st["bytes_per_cycle"] / (t / k) / 1e9 / peak,
+                "vcycle_fused_roofline_frac":
+                    fused_bytes_per_cycle(dim, N, 8, nu, nu, 1, 2, st["bytes_per_cycle"]) / (t / k) / 1e9 / peak}
             del so
         del bd
         torch.cuda.empty_cache()
@@ -522,7 +530,9 @@ def w_sweep(sp, torch, stream, peak):
             "cycles": k, "converged": conv, "time_to_tol_ms": t * 1e3, "ms_per_cycle": t / k * 1e3,
             "dof_per_s": (N - 1) ** dim * k / t, "rho_hat": (hist[-1] / hist[0]) ** (1.0 / k) if k else None,
             "bytes_per_cycle": st["bytes_per_cycle"], "kernels_per_cycle": st["kernels_per_cycle"],
-            "vcycle_roofline_frac": st["bytes_per_cycle"] / (t / k) / 1e9 / peak}
+            "vcycle_roofline_frac": st["bytes_per_cycle"] / (t / k) / 1e9 / peak,
+            "vcycle_fused_roofline_frac":
+                fused_bytes_per_cycle(dim, N, 8, 1, 0, 2, 4, st["bytes_per_cycle"]) / (t / k) / 1e9 / peak}
         del so, bd
         torch.cuda.empty_cache()
     return res
@@ -568,6 +578,26 @@ def api_e2e(sp, torch):
     return res
 
 
+def fused_bytes_per_cycle(dim, N, esize, nu1, nu2, gamma, coarsest_N, bytes_survey):
+    """Bytes the fused schedule has to move per cycle: the SURVEY.md 8d count (every operator
+    reading and writing its vectors once) minus what the two bitwise-safe fusions of the named
+    smoothers never move: the norm's read of (x, b) on the finest level (folded into the first
+    pre-sweep, nu1 >= 1) and the prolonged iterate's write + re-read on the K3 + K1 levels
+    (nu2 >= 1; 2D mesh counts > 2048, 3D >= 256: sweep_pc_supported in kernels_sweep.cu)."""
+    saved, visits, n = 0.0, 1.0, N
+    level = 0
+    while n > coarsest_N:
+        pts = float((n - 1) ** dim)
+        if level == 0 and nu1 >= 1:
+            saved += 2.0 * esize * pts
+        if nu2 >= 1 and ((dim == 2 and n > 2048) or (dim == 3 and n >= 256)):
+            saved += visits * 2.0 * esize * pts
+        visits *= gamma
+        n //= 2
+        level += 1
+    return bytes_survey - saved
+
+
 def microbench(sp, torch, stream, peak):
     """Config 5: each hot kernel in isolation on 16384^2 (2D) and 512^3 (3D), fp64 and fp32.
     Inputs larger than L2; best of reps after warm-up; bytes are the §8d minimal counts."""
@@ -584,8 +614,10 @@ def microbench(sp, torch, stream, peak):
             n = (N - 1) ** dim
             key = f"{dim}d_N{N}_{dtype}"
             r = {}
+            # K3 + K1 (op 6): x + P e and the sweep in one march: x, b, e/2^d in, x' out
             for op, name, bpu in ((0, "sweep", 3.0), (1, "residual_restrict", 2 + 2.0 ** -dim),
-                                  (2, "prolong_correct", 2 + 2.0 ** -dim), (3, "residual_norm", 2.0)):
+                                  (2, "prolong_correct", 2 + 2.0 ** -dim), (3, "residual_norm", 2.0),
+                                  (6, "prolong_correct_sweep", 3 + 2.0 ** -dim)):
                 so.op(op, 5)
                 best = min(time_events(lambda: so.op(op, 5), stream, 5) for _ in range(3))
                 gbs = bpu * s * n / best / 1e9

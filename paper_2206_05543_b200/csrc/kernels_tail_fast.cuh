@@ -169,11 +169,11 @@ struct FastTail {
 
     // entry level in: b (and the start iterate unless the entry is from zero) of the box
     // [-1, n+1)^D of the global padded layout, whose frame is zero.  Compile-time geometry: the
-    // loop is unrolled in batches of 8 points whose global loads are all issued before the first
-    // store (a rolled loop waited out one L2 round trip per iteration).
+    // loop is fully unrolled and every global load is issued before the first store (a rolled
+    // loop waited out one L2 round trip per iteration).
     __device__ static __forceinline__ void load_entry(const TailArgs<T>& a, T* arr, bool fz) {
         constexpr int W0 = w(0), CNT = D == 2 ? W0 * W0 : W0 * W0 * W0;
-        constexpr int IT = (CNT + NT - 1) / NT, UB = 8;
+        constexpr int IT = (CNT + NT - 1) / NT, UB = IT;  // one batch: every load in flight at once
         const long long p0 = D == 2 ? a.gL.px : a.gL.pp;
 #pragma unroll 1
         for (int ib = 0; ib < IT; ib += UB) {
@@ -221,6 +221,7 @@ struct FastTail {
 
     __device__ static __forceinline__ void run(const TailArgs<T>& a, T* arr) {
         const int t = threadIdx.x;
+        if (a.prof && t == 0) a.prof[2 * kTailMaxOps] = clock64();  // kernel entry (SPAIMG_TAIL_PROF)
         load_entry(a, arr, a.entry_fz != 0);
         for (int i = zero_from() + t; i < elems(); i += NT) arr[i] = T(0);
         if constexpr (kDebugChecks) {
@@ -253,6 +254,10 @@ struct FastTail {
         __syncthreads();
         if (a.prof && t == 0) a.prof[pc] = clock64();
         store_entry(a, arr);
+        if (a.prof) {
+            __syncthreads();
+            if (t == 0) a.prof[2 * kTailMaxOps + 1] = clock64();  // kernel exit
+        }
     }
 };
 

@@ -895,6 +895,9 @@ template <class T> struct Solver final : spaimg_solver {
         for (int k = 0; k < 8; ++k)
             if (cnt[k]) fprintf(stderr, "tailprof sum %-7s %3lld ops %8lld cycles\n", names[k], cnt[k], tot[k]);
         fprintf(stderr, "tailprof total %lld cycles\n", c[ops.size()] - c[0]);
+        if (tail_args[0].fast_le)
+            fprintf(stderr, "tailprof entry -> first op %lld cycles, last op -> exit %lld cycles\n",
+                    c[0] - c[2 * kTailMaxOps], c[2 * kTailMaxOps + 1] - c[ops.size()]);
     }
 
     // one visit of the engine's entry level: x[a] updated in place
@@ -1369,6 +1372,10 @@ template <class T> struct Solver final : spaimg_solver {
             }
             case 5:  // two sweeps in one march (2D marching levels)
                 CK(launch_sweep2<T>(L.L, L.x[0], L.b, L.x[1], M, shape, L.sA, L.sM, omega, false, s));
+                return 0;
+            case 6:  // K3 + K1: sweep(x + P e) in one march (levels where sweep_pc_supported)
+                if (!fused || !sweep_pc_supported(L.L, shape)) return fail(SPAIMG_ENOTSUP, "no K3 + K1 march on this level");
+                CK(launch_sweep_pc<T>(L.L, lv[1].L, L.x[0], lv[1].x[0], L.b, L.x[1], M, shape, L.sA, L.sM, omega, s));
                 return 0;
             default: return fail(SPAIMG_EINVAL, "unknown op");
         }

@@ -1,6 +1,7 @@
 """Launch one hot-path kernel in isolation for ncu: python tools/prof_op.py <cfg> <op> [reps] [dtype]
 cfg: c2 (2D 4096^2 m9), c4 (3D 512^3 m7), c5_2d (16384^2 m9), c5_3d (512^3 m7); op: 0 sweep,
-1 residual+restrict, 2 prolong+correct, 3 norm, 4 norm+sweep (part A), 5 two sweeps in one march, 9 = whole
+1 residual+restrict, 2 prolong+correct, 3 norm, 4 norm+sweep (part A), 5 two sweeps in one march,
+6 K3+K1 (prolongation + correction fused into the sweep), 9 = whole
 cycles."""
 import os
 import sys
