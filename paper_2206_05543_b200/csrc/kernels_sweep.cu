@@ -259,11 +259,14 @@ template <class T> struct M2Two {
 };
 
 // One marching step k (row j = q0 + k): r(j) for the strip (+ halo), then output row j-1.
-// P = k mod 6 makes every stage slot and register-row index a compile-time constant.
-template <class T, int S, bool FZ, int NM, int P, bool TW>
+// P = k mod 6 makes every stage slot and register-row index a compile-time constant.  PROD: the
+// producer warp's step (the march loop is instantiated per role, so no step tests the role);
+// EDGE: the strip holds columns outside the interior (column masks compiled in).  orow: the
+// output row pointer of this step (row j-1, own first column), advanced by every step.
+template <class T, int S, bool FZ, int NM, int P, bool TW, bool PROD, bool EDGE>
 __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_vec<T>()], T (&R)[3][m2_vec<T>()],
                                         T (&RL)[3], T (&RH)[3], M2Two<T>& tw, const Terms<T>& M, T sA, T sM, T omega,
-                                        double& nacc) {
+                                        double& nacc, T*& orow) {
     using O = Op<T>;
     constexpr int VEC = m2_vec<T>();
     constexpr int W = m2_width<T>();
@@ -276,7 +279,9 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
     mbar_wait(&c.full[sp], (uint32_t)(((k + 1) / ST) & 1));
     const bool row_in = (unsigned)j < (unsigned)c.n;
     T* rrow = c.rr + rs * RW;
-    if (!c.producer) {
+    T* const dst = orow;
+    orow += c.px;
+    if constexpr (!PROD) {
         T bj[VEC];
         V16<T>::ld(c.bs + sj * RW + c.sidx, bj);
         if constexpr (TW) {
@@ -297,10 +302,13 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
                 R[ic][v] = residual2d<T>(bj[v], X[ic][v], X[ip][v], X[im][v], xe, xw, sA);
             }
         }
-        if (!row_in || c.last_strip || (TW && c.c0 < 0)) {
+        if constexpr (EDGE) {
 #pragma unroll
             for (int v = 0; v < VEC; ++v)
                 if (!row_in || c.col + v >= c.n || (TW && c.col + v < 0)) R[ic][v] = T(0);  // r is zero outside
+        } else if (!row_in) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) R[ic][v] = T(0);
         }
         // ||r||^2 of own rows (TW: strips overlap by VEC columns; the edge consumers do not count)
         if ((NM == 1 || NM == 2) && j >= c.r0 && j < c.r_end && (!TW || (c.tcons > 0 && c.tcons < W / VEC - 1))) {
@@ -308,7 +316,7 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
             for (int v = 0; v < VEC; ++v) nacc += (double)R[ic][v] * (double)R[ic][v];  // ||r||^2, own rows
         }
         if (NM != 2) V16<T>::st(rrow + c.sidx, R[ic]);
-    } else if (NM != 2 && c.lane < 2) {
+    } else if (NM != 2 && c.lane < 2) {  // PROD
         // strip-halo residuals at columns c0-1 (lane 0) and c0+W (lane 1)
         const int si = c.lane == 0 ? VEC - 1 : VEC + W;
         const int cc = c.lane == 0 ? c.c0 - 1 : c.c0 + W;
@@ -323,7 +331,7 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
         rrow[si] = rv;
     }
     named_bar_sync(1, (M2_NW + 1) * 32);
-    if (c.producer) {
+    if constexpr (PROD) {
         // stage j-1 was last read before this barrier: refill its slot with row j-1+ST
         if (c.lane == 0 && j - 1 + ST <= c.q_last) m2_issue<T, S, FZ, NM, TW>(c, j - 1 + ST, sm);
         if constexpr (NM == 3) {  // the strip halos of row j+3 (see m2_correct_row)
@@ -363,8 +371,7 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
         out[v] = relax<T>(FZ ? T(0) : X[im][v], acc, sM, omega);
     }
     if constexpr (!TW) {
-        T* dst = c.orow0 + (long long)(j - 1) * c.px;
-        if (!c.last_strip || c.col + VEC <= c.n) {
+        if (!EDGE || c.col + VEC <= c.n) {
             V16<T>::st(dst, out);
         } else {
 #pragma unroll
@@ -421,13 +428,13 @@ __device__ __forceinline__ void m2_step(const M2Ctx<T>& c, int k, T (&X)[3][m2_v
             }
             // strips overlap by VEC columns on each side: the edge consumers only feed their neighbours
             if (c.tcons > 0 && c.tcons < W / VEC - 1) {
-                T* dst = c.orow0 + (long long)(j - 4) * c.px;
+                T* dst2 = dst - 3 * c.px;  // row j-4
                 if (c.col + VEC <= c.n) {
-                    V16<T>::st(dst, out2);
+                    V16<T>::st(dst2, out2);
                 } else {
 #pragma unroll
                     for (int v = 0; v < VEC; ++v)
-                        if (c.col + v < c.n) dst[v] = out2[v];
+                        if (c.col + v < c.n) dst2[v] = out2[v];
                 }
             }
         }
@@ -514,14 +521,28 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32, TW ? 3 : (NM == 3 ? 5 : 1)) 
     M2Two<T> tw;
     // steps k = 1 .. K: rows j = q0+1 .. r_end (+3 with TW, whose second sweep trails by 3 rows)
     const int K = r_end + (TW ? 3 : 0) - c.q0;
-    for (int kb = 0; kb <= K; kb += ST) {
-        if (kb >= 1) m2_step<T, S, FZ, NM, 0, TW>(c, kb, X, R, RL, RH, tw, M, sA, sM, omega, nacc);
-        if (kb + 1 <= K) m2_step<T, S, FZ, NM, 1, TW>(c, kb + 1, X, R, RL, RH, tw, M, sA, sM, omega, nacc);
-        if (kb + 2 <= K) m2_step<T, S, FZ, NM, 2, TW>(c, kb + 2, X, R, RL, RH, tw, M, sA, sM, omega, nacc);
-        if (kb + 3 <= K) m2_step<T, S, FZ, NM, 3, TW>(c, kb + 3, X, R, RL, RH, tw, M, sA, sM, omega, nacc);
-        if (kb + 4 <= K) m2_step<T, S, FZ, NM, 4, TW>(c, kb + 4, X, R, RL, RH, tw, M, sA, sM, omega, nacc);
-        if (kb + 5 <= K) m2_step<T, S, FZ, NM, 5, TW>(c, kb + 5, X, R, RL, RH, tw, M, sA, sM, omega, nacc);
+    T* orow = c.orow0 + (long long)c.q0 * c.px;  // step k = 1 writes row j-1 = q0
+    // one march loop per role (and, for the consumers, per strip kind), so that no step tests
+    // the role or carries column masks it does not need
+#define M2_MARCH(PROD, EDGE)                                                                                    \
+    for (int kb = 0; kb <= K; kb += ST) {                                                                       \
+        if (kb >= 1) m2_step<T, S, FZ, NM, 0, TW, PROD, EDGE>(c, kb, X, R, RL, RH, tw, M, sA, sM, omega, nacc, orow);         \
+        if (kb + 1 <= K) m2_step<T, S, FZ, NM, 1, TW, PROD, EDGE>(c, kb + 1, X, R, RL, RH, tw, M, sA, sM, omega, nacc, orow); \
+        if (kb + 2 <= K) m2_step<T, S, FZ, NM, 2, TW, PROD, EDGE>(c, kb + 2, X, R, RL, RH, tw, M, sA, sM, omega, nacc, orow); \
+        if (kb + 3 <= K) m2_step<T, S, FZ, NM, 3, TW, PROD, EDGE>(c, kb + 3, X, R, RL, RH, tw, M, sA, sM, omega, nacc, orow); \
+        if (kb + 4 <= K) m2_step<T, S, FZ, NM, 4, TW, PROD, EDGE>(c, kb + 4, X, R, RL, RH, tw, M, sA, sM, omega, nacc, orow); \
+        if (kb + 5 <= K) m2_step<T, S, FZ, NM, 5, TW, PROD, EDGE>(c, kb + 5, X, R, RL, RH, tw, M, sA, sM, omega, nacc, orow); \
     }
+    if (c.producer) {
+        M2_MARCH(true, true)
+    } else if (TW || c.last_strip) {
+        M2_MARCH(false, true)
+    } else {
+        if constexpr (!TW) {
+            M2_MARCH(false, false)
+        }
+    }
+#undef M2_MARCH
     if (NM == 1 || NM == 2) norm_epilogue(nacc, no);
 }
 
@@ -624,8 +645,14 @@ static int pc3_min_n() {
     const char* e = getenv("SPAIMG_PC3_N");  // read per solver plan (host side, not per launch in a graph)
     return e ? atoi(e) : 256;
 }
+// SPAIMG_PC2_N: the smallest 2D mesh count that uses the fused march (default 4096; the level
+// must be a marching level)
+static int pc2_min_n() {
+    const char* e = getenv("SPAIMG_PC2_N");
+    return e ? atoi(e) : 4096;
+}
 bool sweep_pc_supported(const Layout& L, int shape) {
-    if (L.dim == 2) return L.N > 2048;
+    if (L.dim == 2) return pc2_min_n() > 0 && L.N >= pc2_min_n() && L.N > flat_threshold(2);
     return pc3_min_n() > 0 && L.N >= pc3_min_n() && L.N > flat_threshold(3) && (shape == SHAPE_C1 || shape == SHAPE_STAR7);
 }
 
