@@ -21,7 +21,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_checked_build_bitwise(mode, rep):
     env = dict(os.environ, SPAIMG_DEBUG="1")
     if mode == "march":
-        env.update(SPAIMG_FLAT_N2="0", SPAIMG_FLAT_N3="0")
+        # ... and the K3 + K1 marches (in-place correction of the staged rows / planes) on every level
+        env.update(SPAIMG_FLAT_N2="0", SPAIMG_FLAT_N3="0", SPAIMG_PC2_N="1", SPAIMG_PC3_N="1")
     code = ("import runpy, sys; sys.argv = ['sanitize_case']; "
             "from paper_2206_05543_b200 import _lib; lib = _lib.load(); "
             "assert _lib.LIB_PATH.endswith('libspaimg_cuda_debug.so'), _lib.LIB_PATH; "

@@ -295,20 +295,22 @@ def test_alternate_paths_bitwise(env):
         assert sha == hashlib.sha256(uo.tobytes()).hexdigest(), case
 
 
-@pytest.mark.parametrize("env", [{"SPAIMG_PC3_N": "1", "SPAIMG_FLAT_N3": "0"}, {"SPAIMG_PC3_N": "1", "SPAIMG_NO_GRAPH": "1"},
-                                 {"SPAIMG_PC3_N": "0"}],
+@pytest.mark.parametrize("env", [{"SPAIMG_PC3_N": "1", "SPAIMG_PC2_N": "1", "SPAIMG_FLAT_N3": "0", "SPAIMG_FLAT_N2": "0"},
+                                 {"SPAIMG_PC3_N": "1", "SPAIMG_PC2_N": "1", "SPAIMG_NO_GRAPH": "1"},
+                                 {"SPAIMG_PC3_N": "0", "SPAIMG_PC2_N": "0"}],
                          ids=lambda e: ",".join(f"{k[7:]}={v}" for k, v in e.items()))
-def test_pc3_ragged_vs_oracle(env):
-    """3D K3 + K1 plane march (prolongation + correction fused into the first post-sweep) on every
-    level the switches allow -- ragged tile edges, boundary tiles, odd chunk lengths, fp64 and
-    fp32, C1 and STAR7 -- bitwise against the C oracle; SPAIMG_PC3_N=0 is the unfused K3 then K1."""
+def test_pc_ragged_vs_oracle(env):
+    """The K3 + K1 marches (prolongation + correction fused into the first post-sweep; 2D row
+    march, 3D plane march) on every level the switches allow -- ragged strip / tile edges, boundary
+    tiles, odd chunk lengths, fp64 and fp32, every named shape -- bitwise against the C oracle;
+    SPAIMG_PC*_N=0 is the unfused K3 then K1."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, os.path.join(root, "tests", "pc3_case.py")], capture_output=True, text=True,
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "pc_case.py")], capture_output=True, text=True,
                        timeout=900, env=dict(os.environ, **env))
-    assert r.returncode == 0 and "PC3 OK" in r.stdout, (r.stdout[-2000:], r.stderr[-3000:])
+    assert r.returncode == 0 and "PC OK" in r.stdout, (r.stdout[-2000:], r.stderr[-3000:])
 
 
 @pytest.mark.parametrize("dim,N,sm", [(2, 256, "m9"), (2, 4096, "m9"), (2, 512, "jacobi2d"), (3, 64, "m7"),
