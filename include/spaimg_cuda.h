@@ -155,7 +155,10 @@ SPAIMG_API int spaimg_solver_solve_batch(spaimg_solver *s, int nrhs, const void 
 
 /* Isolated kernel launches on the solver's finest-level buffers, for per-operator timing
  * (BASELINE.json config 5): op 0 = fused sweep (K1), 1 = residual+restriction (K2),
- * 2 = prolongation+correction (K3), 3 = residual norm (K4).  `reps` back-to-back launches. */
+ * 2 = prolongation+correction (K3), 3 = residual norm (K4), 4 = norm + first pre-sweep (part A of
+ * the solve loop), 5 = two sweeps in one march (2D marching levels, C1 / STAR5 shapes),
+ * 6 = prolongation+correction fused into the sweep (K3+K1; SPAIMG_ENOTSUP where the level does
+ * not use it).  `reps` back-to-back launches, replayed from a cached graph. */
 SPAIMG_API int spaimg_solver_op(spaimg_solver *s, int op, int reps, void *stream);
 
 #ifdef __cplusplus
