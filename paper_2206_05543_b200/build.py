@@ -20,8 +20,8 @@ LIB = os.path.join(PKG, "libspaimg_cuda.so")
 # loaded instead of LIB when SPAIMG_DEBUG=1
 LIB_DEBUG = os.path.join(PKG, "libspaimg_cuda_debug.so")
 
-SOURCES = ["kernels_basic.cu", "kernels_sweep.cu", "kernels_sweep3d.cu", "kernels_restrict.cu", "kernels_tail.cu", "kernels_tail_fast2d.cu", "kernels_tail_fast3d.cu", "kernels_flat.cu", "kernels_rng.cu", "solver.cu"]
-HEADERS = ["spaimg_common.cuh", "kernels.h", "ptx.cuh", "march.cuh", "tail_ops.cuh", "kernels_tail_fast.cuh"]
+SOURCES = ["kernels_basic.cu", "kernels_sweep.cu", "kernels_sweep_pc.cu", "kernels_sweep2.cu", "kernels_sweep3d.cu", "kernels_restrict.cu", "kernels_tail.cu", "kernels_tail_fast2d.cu", "kernels_tail_fast3d.cu", "kernels_flat.cu", "kernels_rng.cu", "solver.cu"]
+HEADERS = ["spaimg_common.cuh", "kernels.h", "ptx.cuh", "march.cuh", "sweep2d_march.cuh", "tail_ops.cuh", "kernels_tail_fast.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
