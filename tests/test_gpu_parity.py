@@ -329,6 +329,32 @@ def test_fp32_cycles_vs_oracle(dim, N, sm):
     assert np.array_equal(got, ref)
 
 
+def test_long_histories_grow_on_demand():
+    """max_iters beyond the initial history capacity (the reference accepts any max_iters,
+    multigrid.py:196-201; round 1 capped it at 4096), and more Solver.cycles() than the history
+    held: the device history grows, nothing is overwritten, and the start of the history still
+    equals the oracle's."""
+    N = 16
+    b = np.random.default_rng(5).uniform(-1, 1, (N - 1, N - 1))
+    M = sp.named("jacobi2d")
+    cfg = sp.MgConfig(smoother=M, cycle="V", nu1=1, nu2=0, coarsest_N=2, tol=1e-300, max_iters=5000)
+    u, rep = sp.solve(sp.Grid(N, dev(b)), cfg, u0=0)
+    assert rep.iterations == 5000 and not rep.converged and len(rep.residual_norms) == 5001
+    _, norms, _, _ = c_oracle.solve_history(b, N, npo.terms_of(M.stencil), M.omega_opt_analytic, 1, 0, 1, 2,
+                                            tol=1e-300, max_iters=40)
+    assert max(abs(a - r) / r for a, r in zip(rep.residual_norms[:41], norms)) < 1e-8
+    so = sp.Solver(cfg, 2, N)
+    so.load(dev(b))
+    so.cycles(300)   # past the 101 norms allocated at creation
+    so.cycles(300)
+    got = torch.empty((N - 1, N - 1), dtype=torch.float64, device="cuda")
+    so.store(got)
+    ref = np.zeros_like(b)
+    for _ in range(600):
+        ref = c_oracle.cycle(ref, b, N, npo.terms_of(M.stencil), M.omega_opt_analytic, 1, 0, 1, 2)
+    assert np.array_equal(got.cpu().numpy(), ref)
+
+
 @pytest.mark.parametrize("seed,shape,dtype", [(0, (4095, 4095), torch.float64), (1, (127, 127, 127), torch.float64),
                                               (12345, (17, 33), torch.float32), (7, (1,), torch.float64)])
 def test_device_uniform_is_numpy_bitwise(seed, shape, dtype):
