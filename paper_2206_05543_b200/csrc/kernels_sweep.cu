@@ -26,19 +26,14 @@ __global__ void __launch_bounds__(256) k_sweep2d_tile(Layout L, const T* __restr
     __shared__ T rs[RH * RW];
     const int c0 = blockIdx.x * S2_TW, r0 = blockIdx.y * S2_TH;
     const int n = L.n;
-    for (int q = threadIdx.x; q < RH * RW; q += blockDim.x) {
-        const int i0 = r0 - 1 + q / RW, i1 = c0 - 1 + q % RW;
-        T rv = T(0);
-        if (i0 >= 0 && i0 < n && i1 >= 0 && i1 < n) {
-            const long long p = pidx2(L, i0, i1);
-            if constexpr (FZ) {
-                rv = b[p];  // b - A 0 == b exactly
-            } else {
-                rv = residual2d<T>(b[p], x[p], x[p + L.px], x[p - L.px], x[p + 1], x[p - 1], sA);
-            }
-        }
-        rs[q] = rv;
-    }
+    flat_stage_r<T, 2, FZ, RH * RW, 256, 3>(
+        x, b, L, sA,
+        [&](int q, long long& p) {
+            const int i0 = r0 - 1 + q / RW, i1 = c0 - 1 + q % RW;
+            p = pidx2(L, i0, i1);
+            return (i0 >= 0) & (i0 < n) & (i1 >= 0) & (i1 < n);
+        },
+        [&](int q, T rv) { rs[q] = rv; });
     __syncthreads();
     for (int q = threadIdx.x; q < S2_TH * S2_TW; q += blockDim.x) {
         const int a0 = q / S2_TW, a1 = q % S2_TW;
@@ -65,20 +60,14 @@ __global__ void __launch_bounds__(256) k_sweep3d_tile(Layout L, const T* __restr
     __shared__ T rs[RZ * RY * RX];
     const int x0 = blockIdx.x * S3_TX, y0 = blockIdx.y * S3_TY, z0 = blockIdx.z * S3_TZ;
     const int n = L.n;
-    for (int q = threadIdx.x; q < RZ * RY * RX; q += blockDim.x) {
-        const int i0 = z0 - 1 + q / (RY * RX), i1 = y0 - 1 + (q / RX) % RY, i2 = x0 - 1 + q % RX;
-        T rv = T(0);
-        if (i0 >= 0 && i0 < n && i1 >= 0 && i1 < n && i2 >= 0 && i2 < n) {
-            const long long p = pidx3(L, i0, i1, i2);
-            if constexpr (FZ) {
-                rv = b[p];
-            } else {
-                rv = residual3d<T>(b[p], x[p], x[p + L.pp], x[p - L.pp], x[p + L.px], x[p - L.px], x[p + 1], x[p - 1],
-                                   sA);
-            }
-        }
-        rs[q] = rv;
-    }
+    flat_stage_r<T, 3, FZ, RZ * RY * RX, 256, 3>(
+        x, b, L, sA,
+        [&](int q, long long& p) {
+            const int i0 = z0 - 1 + q / (RY * RX), i1 = y0 - 1 + (q / RX) % RY, i2 = x0 - 1 + q % RX;
+            p = pidx3(L, i0, i1, i2);
+            return (i0 >= 0) & (i0 < n) & (i1 >= 0) & (i1 < n) & (i2 >= 0) & (i2 < n);
+        },
+        [&](int q, T rv) { rs[q] = rv; });
     __syncthreads();
     for (int q = threadIdx.x; q < S3_TZ * S3_TY * S3_TX; q += blockDim.x) {
         const int a0 = q / (S3_TY * S3_TX), a1 = (q / S3_TX) % S3_TY, a2 = q % S3_TX;

@@ -76,6 +76,70 @@ __device__ __forceinline__ T pick(const T* rm, const T* rc, const T* rp, T lm, T
 template <class T>
 __device__ __forceinline__ void stg16(T* p, const T* v) { V16<T>::st(p, v); }
 
+// Flat tile kernels: stage r = b - A x (FZ: r = b, the iterate is zero) at CNT points of a tile
+// footprint, NTH threads, in groups of BATCH points per thread whose global loads are all issued
+// before the first use.  (The rolled per-point loop these kernels started with paid one L2 round
+// trip per point: bounds branch, 6-8 dependent-on-nothing loads, arithmetic, store, next point.)
+//   idx(q, p): footprint point q -> true and its element offset p when it is an interior point
+//   put(q, r): store the residual of footprint point q (zero outside the interior)
+// Out-of-range points load from the interior origin (always addressable) and discard the value.
+template <class T, int D, bool FZ, int CNT, int NTH, int BATCH, class Idx, class Put>
+__device__ __forceinline__ void flat_stage_r(const T* __restrict__ x, const T* __restrict__ b, const Layout& L, T sA,
+                                             Idx idx, Put put) {
+    constexpr int IT = (CNT + NTH - 1) / NTH;
+    constexpr int NL = FZ ? 1 : (D == 2 ? 6 : 8);
+#pragma unroll
+    for (int i0 = 0; i0 < IT; i0 += BATCH) {
+        T v[BATCH][NL];
+        bool ok[BATCH];
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u) {
+            ok[u] = false;
+            if (i0 + u < IT) {
+                // branch-free: every load of the group must be issuable before the first use
+                const int q = (i0 + u) * NTH + (int)threadIdx.x;
+                long long p = L.origin;
+                const bool in = idx(q, p);
+                ok[u] = ((i0 + u + 1) * NTH <= CNT || q < CNT) & in;
+                p = ok[u] ? p : L.origin;
+                v[u][0] = b[p];
+                if constexpr (!FZ) {
+                    v[u][1] = x[p];
+                    if constexpr (D == 2) {
+                        v[u][2] = x[p + L.px];
+                        v[u][3] = x[p - L.px];
+                        v[u][4] = x[p + 1];
+                        v[u][5] = x[p - 1];
+                    } else {
+                        v[u][2] = x[p + L.pp];
+                        v[u][3] = x[p - L.pp];
+                        v[u][4] = x[p + L.px];
+                        v[u][5] = x[p - L.px];
+                        v[u][6] = x[p + 1];
+                        v[u][7] = x[p - 1];
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u) {
+            if (i0 + u < IT) {
+                const int q = (i0 + u) * NTH + (int)threadIdx.x;
+                T rv;
+                if constexpr (FZ) {
+                    rv = v[u][0];  // b - A 0 == b exactly
+                } else if constexpr (D == 2) {
+                    rv = residual2d<T>(v[u][0], v[u][1], v[u][2], v[u][3], v[u][4], v[u][5], sA);
+                } else {
+                    rv = residual3d<T>(v[u][0], v[u][1], v[u][2], v[u][3], v[u][4], v[u][5], v[u][6], v[u][7], sA);
+                }
+                rv = ok[u] ? rv : T(0);
+                if ((i0 + u + 1) * NTH <= CNT || q < CNT) put(q, rv);
+            }
+        }
+    }
+}
+
 // Chunk count along the marching axis for `tiles` CTAs per chunk row and `slots` resident CTA
 // slots: favour a whole number of waves (a partial last wave leaves most SMs idle while a few
 // CTAs march their whole chunk) while amortising each chunk's pipeline fill (`fill` extra
