@@ -490,6 +490,14 @@ template <class T> struct Solver final : spaimg_solver {
     bool in_solve_graph = false;
 
     int init(const spaimg_mg_config& c) {
+        {   // the direct solve keeps the coarse vector in one CTA's shared memory (k_coarse_solve)
+            int dev = 0, optin = 0;
+            CK(cudaGetDevice(&dev));
+            CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+            if ((size_t)c.coarse_n * sizeof(T) > (size_t)optin)
+                return fail(SPAIMG_ENOTSUP, "coarse system of " + std::to_string(c.coarse_n) + " unknowns exceeds the direct solve's limit of " +
+                                                std::to_string(optin / (int)sizeof(T)) + " (choose a smaller coarsest_N)");
+        }
         cfg = c;
         lu_h.assign(c.coarse_lu, c.coarse_lu + (size_t)c.coarse_n * c.coarse_n);
         piv_h.assign(c.coarse_piv, c.coarse_piv + c.coarse_n);

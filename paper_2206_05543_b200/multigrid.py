@@ -362,6 +362,12 @@ def _mg_struct(cfg: MgConfig, dim: int, N: int, dtype_code: int):
         if M.dim != dim:
             raise ValueError(f"smoother dim {M.dim} != grid dim {dim}")
     Nc = _coarse_level(N, cfg.coarsest_N)
+    # the device direct solve (K5) keeps the coarse vector in one CTA's shared memory: refuse a
+    # larger coarsest level here, before factorising it (the library checks again)
+    n_coarse = (Nc - 1) ** dim
+    if n_coarse * (8 if dtype_code == _lib.F64 else 4) > 227 * 1024:
+        raise _lib.SpaimgError(f"coarsest level N={Nc} has {n_coarse} unknowns, more than the device direct solve "
+                               "holds; choose a smaller coarsest_N")
     lu, piv = _coarsest_lu(dim, Nc)
     c = _lib.SpaimgMgConfig()
     c.dtype = dtype_code

@@ -329,6 +329,30 @@ def test_fp32_cycles_vs_oracle(dim, N, sm):
     assert np.array_equal(got, ref)
 
 
+@pytest.mark.parametrize("seed", [1, 2])
+def test_random_configs_vs_oracle(seed):
+    """Seeded random sweep over the whole cycle path (tests/fuzz_case.py): ragged sizes, every named
+    smoother, V / W, nu in 0..2, coarsest_N along the halving chain, fp64 / fp32 and random
+    settings of every path switch, two cycles each, bitwise against the C oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "fuzz_case.py"), str(seed), "60"],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "FUZZ OK" in r.stdout, (r.stdout[-1500:], r.stderr[-3000:])
+
+
+def test_oversized_coarse_system_is_refused():
+    """A coarsest level whose unknowns do not fit the single-CTA direct solve is refused with a
+    message when the solver is planned (before the LU is even factorised), not with a launch
+    failure inside a cycle."""
+    from paper_2206_05543_b200._lib import SpaimgError
+    cfg = sp.MgConfig(smoother=sp.named("jacobi3d"), cycle="V", nu1=1, nu2=1, coarsest_N=33)
+    with pytest.raises(SpaimgError, match="unknowns"):
+        sp.Solver(cfg, 3, 66)
+
+
 def test_long_histories_grow_on_demand():
     """max_iters beyond the initial history capacity (the reference accepts any max_iters,
     multigrid.py:196-201; round 1 capped it at 4096), and more Solver.cycles() than the history
