@@ -80,5 +80,43 @@ def main(seed, ncases):
     print("FUZZ OK")
 
 
+def operators(seed, ncases):
+    """The per-operator entry points (smooth with 0..3 steps incl. odd mesh counts, residual +
+    restriction, prolongation + correction, residual norm) at random sizes, host and device
+    arrays, fp64 and fp32, bitwise against the C oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    for case in range(ncases):
+        dim = int(rng.choice([2, 3]))
+        N = int(rng.integers(3, 700)) if dim == 2 else int(rng.integers(3, 90))
+        dtype = str(rng.choice(["float64", "float32"]))
+        side = str(rng.choice(["host", "device"]))
+        if side == "host":
+            dtype = "float64"  # host grids are float64 like the reference's (grids.py:24)
+        npdt = np.float64 if dtype == "float64" else np.float32
+        tdt = torch.float64 if dtype == "float64" else torch.float32
+        sm = str(rng.choice([k for k in sp.NAMED_SMOOTHER_IDS if sp.named(k).dim == dim]))
+        M = sp.named(sm)
+        mt = npo.terms_of(M.stencil)
+        steps = int(rng.integers(0, 4))
+        x = rng.uniform(-1, 1, (N - 1,) * dim).astype(npdt)
+        b = rng.uniform(-1, 1, (N - 1,) * dim).astype(npdt)
+        wrap = (lambda a: a) if side == "host" else (lambda a: torch.as_tensor(a).to("cuda", tdt))
+        host = lambda g: g.values.cpu().numpy() if torch.is_tensor(g.values) else g.values  # noqa: E731
+        print("op case", case, dim, N, sm, steps, dtype, side, flush=True)
+        u, bb = sp.Grid(N, wrap(x)), sp.Grid(N, wrap(b))
+        got = host(sp.smooth(u, bb, M.stencil, M.omega_opt_analytic, steps))
+        assert np.array_equal(got, c_oracle.smooth(x, b, N, mt, M.omega_opt_analytic, steps, dtype=npdt)), "smooth"
+        assert sp.residual_norm(u, bb) == __import__("pytest").approx(c_oracle.residual_norm(x, b, N, dtype=npdt), rel=1e-12)
+        if N % 2 == 0 and N >= 4:
+            e = rng.uniform(-1, 1, (N // 2 - 1,) * dim).astype(npdt)
+            assert np.array_equal(host(sp.residual_restrict(u, bb)), c_oracle.residual_restrict(x, b, N, dtype=npdt)), "rr"
+            assert np.array_equal(host(sp.prolong_correct(u, sp.Grid(N // 2, wrap(e)))),
+                                  c_oracle.prolong_correct(x, e, dtype=npdt)), "pc"
+    print("FUZZ OK")
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 3 and sys.argv[3] == "ops":
+        operators(int(sys.argv[1]), int(sys.argv[2]))
+        sys.exit(0)
     main(int(sys.argv[1]) if len(sys.argv) > 1 else 0, int(sys.argv[2]) if len(sys.argv) > 2 else 24)

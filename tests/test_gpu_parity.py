@@ -343,6 +343,19 @@ def test_random_configs_vs_oracle(seed):
     assert r.returncode == 0 and "FUZZ OK" in r.stdout, (r.stdout[-1500:], r.stderr[-3000:])
 
 
+def test_random_operators_vs_oracle():
+    """Seeded random sweep over the per-operator entry points (tests/fuzz_case.py operators): smooth
+    with 0..3 steps at odd and even mesh counts, residual + restriction, prolongation + correction
+    and the residual norm, host and device arrays, fp64 and fp32, bitwise against the C oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "fuzz_case.py"), "0", "60", "ops"],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "FUZZ OK" in r.stdout, (r.stdout[-1500:], r.stderr[-3000:])
+
+
 def test_oversized_coarse_system_is_refused():
     """A coarsest level whose unknowns do not fit the single-CTA direct solve is refused with a
     message when the solver is planned (before the LU is even factorised), not with a launch
