@@ -18,14 +18,18 @@ __device__ __forceinline__ long long pidx3(const Layout& L, int i0, int i1, int 
 constexpr int S2_TW = 64, S2_TH = 16;
 constexpr int S3_TX = 32, S3_TY = 8, S3_TZ = 4;
 
-template <class T, int S, bool FZ>
+// NORM: ||b - A x||^2 of the INPUT iterate over the tile's own points joins the deterministic
+// norm reduction (march.cuh norm_epilogue): part A of the solve loop on flat-sized finest levels
+template <class T, int S, bool FZ, bool NORM = false>
 __global__ void __launch_bounds__(256) k_sweep2d_tile(Layout L, const T* __restrict__ x, const T* __restrict__ b,
-                                                      T* __restrict__ xo, Terms<T> M, T sA, T sM, T omega) {
+                                                      T* __restrict__ xo, Terms<T> M, T sA, T sM, T omega,
+                                                      NormOut no) {
     using O = Op<T>;
     constexpr int RW = S2_TW + 2, RH = S2_TH + 2;
     __shared__ T rs[RH * RW];
     const int c0 = blockIdx.x * S2_TW, r0 = blockIdx.y * S2_TH;
     const int n = L.n;
+    double nacc = 0.0;
     flat_stage_r<T, 2, FZ, RH * RW, 256, 3>(
         x, b, L, sA,
         [&](int q, long long& p) {
@@ -33,7 +37,13 @@ __global__ void __launch_bounds__(256) k_sweep2d_tile(Layout L, const T* __restr
             p = pidx2(L, i0, i1);
             return (i0 >= 0) & (i0 < n) & (i1 >= 0) & (i1 < n);
         },
-        [&](int q, T rv) { rs[q] = rv; });
+        [&](int q, T rv) {
+            rs[q] = rv;
+            if constexpr (NORM) {
+                const int lr = q / RW, lc = q % RW;  // the one-point ring belongs to the neighbour tiles
+                if (lr >= 1 && lr <= S2_TH && lc >= 1 && lc <= S2_TW) nacc += (double)rv * (double)rv;
+            }
+        });
     __syncthreads();
     for (int q = threadIdx.x; q < S2_TH * S2_TW; q += blockDim.x) {
         const int a0 = q / S2_TW, a1 = q % S2_TW;
@@ -50,16 +60,19 @@ __global__ void __launch_bounds__(256) k_sweep2d_tile(Layout L, const T* __restr
         const long long p = pidx2(L, i0, i1);
         xo[p] = relax<T>(FZ ? T(0) : x[p], acc, sM, omega);
     }
+    if constexpr (NORM) norm_epilogue(nacc, no);
 }
 
-template <class T, int S, bool FZ>
+template <class T, int S, bool FZ, bool NORM = false>
 __global__ void __launch_bounds__(256) k_sweep3d_tile(Layout L, const T* __restrict__ x, const T* __restrict__ b,
-                                                      T* __restrict__ xo, Terms<T> M, T sA, T sM, T omega) {
+                                                      T* __restrict__ xo, Terms<T> M, T sA, T sM, T omega,
+                                                      NormOut no) {
     using O = Op<T>;
     constexpr int RX = S3_TX + 2, RY = S3_TY + 2, RZ = S3_TZ + 2;
     __shared__ T rs[RZ * RY * RX];
     const int x0 = blockIdx.x * S3_TX, y0 = blockIdx.y * S3_TY, z0 = blockIdx.z * S3_TZ;
     const int n = L.n;
+    double nacc = 0.0;
     flat_stage_r<T, 3, FZ, RZ * RY * RX, 256, 3>(
         x, b, L, sA,
         [&](int q, long long& p) {
@@ -67,7 +80,14 @@ __global__ void __launch_bounds__(256) k_sweep3d_tile(Layout L, const T* __restr
             p = pidx3(L, i0, i1, i2);
             return (i0 >= 0) & (i0 < n) & (i1 >= 0) & (i1 < n) & (i2 >= 0) & (i2 < n);
         },
-        [&](int q, T rv) { rs[q] = rv; });
+        [&](int q, T rv) {
+            rs[q] = rv;
+            if constexpr (NORM) {
+                const int lz = q / (RY * RX), ly = (q / RX) % RY, lx = q % RX;
+                if (lz >= 1 && lz <= S3_TZ && ly >= 1 && ly <= S3_TY && lx >= 1 && lx <= S3_TX)
+                    nacc += (double)rv * (double)rv;
+            }
+        });
     __syncthreads();
     for (int q = threadIdx.x; q < S3_TZ * S3_TY * S3_TX; q += blockDim.x) {
         const int a0 = q / (S3_TY * S3_TX), a1 = (q / S3_TX) % S3_TY, a2 = q % S3_TX;
@@ -84,6 +104,7 @@ __global__ void __launch_bounds__(256) k_sweep3d_tile(Layout L, const T* __restr
         const long long p = pidx3(L, i0, i1, i2);
         xo[p] = relax<T>(FZ ? T(0) : x[p], acc, sM, omega);
     }
+    if constexpr (NORM) norm_epilogue(nacc, no);
 }
 
 bool sweep_fused_supported(int dim, int shape) {
@@ -100,17 +121,18 @@ template <class T, int S, bool FZ, int NM>
 static cudaError_t sweep_dispatch(const Layout& L, const T* x, const T* b, T* xo, const Terms<T>& M, T sA, T sM,
                                   T omega, const NormOut& no, cudaStream_t s) {
     constexpr int S3 = (S == SHAPE_GENERIC || S == SHAPE_C1 || S == SHAPE_STAR7) ? S : SHAPE_GENERIC;
-    const bool flat = NM == 0 && L.N <= flat_threshold(L.dim);
+    // flat-sized levels: the tile kernels (with the norm when this is part A of the solve loop)
+    const bool flat = (NM == 0 || NM == 1) && L.N <= flat_threshold(L.dim);
     if (L.dim == 2) {
-        if (flat && NM == 0) {
+        if (flat) {
             dim3 g((L.n + S2_TW - 1) / S2_TW, (L.n + S2_TH - 1) / S2_TH);
-            return launch_k(k_sweep2d_tile<T, S, FZ>, g, dim3(256), 0, s, L, x, b, xo, M, sA, sM, omega);
+            return launch_k(k_sweep2d_tile<T, S, FZ, NM == 1>, g, dim3(256), 0, s, L, x, b, xo, M, sA, sM, omega, no);
         }
         return launch_sweep2d_march<T, S, FZ, NM>(L, x, b, xo, M, sA, sM, omega, no, s);
     }
-    if (flat && NM == 0) {
+    if (flat) {
         dim3 g((L.n + S3_TX - 1) / S3_TX, (L.n + S3_TY - 1) / S3_TY, (L.n + S3_TZ - 1) / S3_TZ);
-        return launch_k(k_sweep3d_tile<T, S, FZ>, g, dim3(256), 0, s, L, x, b, xo, M, sA, sM, omega);
+        return launch_k(k_sweep3d_tile<T, S, FZ, NM == 1>, g, dim3(256), 0, s, L, x, b, xo, M, sA, sM, omega, no);
     }
     return launch_sweep3d_march<T, S3, FZ, NM>(L, x, b, xo, M, sA, sM, omega, no, s);
 }

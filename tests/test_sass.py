@@ -4,7 +4,8 @@ where they are part of the contract or off the iterate path:
   * the coarse LU solve (getrs order with FMA, Appendix A.6, and the correctly rounded pivot
     division): k_coarse_solve, k_tail, k_tail_fast;
   * the residual norm's sqrt (IEEE-rounded sqrt uses DFMA internally; the norm never feeds back):
-    the Mode 1/2 (norm) instantiations of the marching kernels, k_residual_norm.
+    the Mode 1/2 (norm) instantiations of the marching kernels, the NORM variants of the flat
+    tile sweeps, k_residual_norm.
 Runs on the CPU with cuobjdump on the in-tree library."""
 import os
 import re
@@ -40,6 +41,9 @@ def _allowed(name):
     m = re.match(r"void spaimg::k_sweep(2d|3d)_march<\w+, \d+, (true|false), (\d)(, (true|false))?>", name)
     if m:
         return m.group(3) in ("1", "2")  # norm modes
+    m = re.match(r"void spaimg::k_sweep(2d|3d)_tile<\w+, \d+, (true|false), (true|false)>", name)
+    if m:
+        return m.group(3) == "true"  # the flat sweep's norm variant (NORM = true)
     return False
 
 
